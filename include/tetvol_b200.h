@@ -1,0 +1,227 @@
+/* tetvol_b200 — B200-native (sm_100a) renderer and LEB builder for adaptive
+ * tetrahedral grids, behind a plain C ABI.
+ *
+ * Drop-in boundary. Each entry point replaces one call of the reference C++
+ * API (paths relative to /root/reference/proj):
+ *
+ *   tv_grid_upload      <- a TetGrid value as produced by TetGrid::init_roots /
+ *                          build_adaptive_grid / load_grid: its pools
+ *                          vertices(), tets(), roots() (tet_grid.hpp:118-122)
+ *   tv_grid_download    -> TetGrid::assemble(...) input (tet_grid.hpp:110-111)
+ *   tv_build            <- build_adaptive_grid(vol, cfg, camera, stats)
+ *                          (builder.hpp:51-52)
+ *   tv_render           <- render(grid, camera, cfg, threads) (tracer.hpp:84-85)
+ *   tv_render_tiles     <- the per-rank share of render() for multi-GPU
+ *                          image-space sharding (interleaved 16x16 tiles)
+ *   tv_march_segments   <- march_segments(grid, ray, stats) (tracer.hpp:49)
+ *   tv_locate_points    <- TetGrid::locate_point (tet_grid.hpp:166)
+ *   tv_render_regular   <- render_reference(RegularGrid::from_volume(vol, s),
+ *                          camera, cfg) (regular_grid.hpp:66-67)
+ *
+ * Conventions: no C++ exception crosses this boundary; every function returns
+ * a tv_status (0 = TV_OK) and tv_last_error() holds a thread-local message.
+ * Handles are opaque and owned by the caller (free with tv_grid_free).
+ * Pointers are HOST pointers unless the name says _dev. Device work runs on
+ * the grid's device; functions taking a `stream` run asynchronously on it
+ * (0 = the legacy default stream) and otherwise synchronise before returning.
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point returns TV_ERR_CUDA.
+ */
+#ifndef TETVOL_B200_H
+#define TETVOL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TV_NO_TET 0xffffffffu
+
+typedef enum {
+    TV_OK = 0,
+    TV_ERR = 1,         /* runtime failure (reference: std::runtime_error)            */
+    TV_ERR_CONFIG = 2,  /* ConfigError (tracer.cpp:131-141, builder.cpp:12-17)         */
+    TV_ERR_CAMERA = 3,  /* CameraError (camera.cpp:15-20)                             */
+    TV_ERR_GRID = 4,    /* GridError family (tet_grid.hpp:24-38)                      */
+    TV_ERR_OUTSIDE = 5, /* OutsideGrid (tet_grid.hpp:33-35)                           */
+    TV_ERR_CUDA = 6,    /* no device, launch or copy failure                          */
+    TV_ERR_OOM = 7,     /* device allocation failed                                   */
+    TV_ERR_ARG = 8      /* null pointer / size mismatch at the ABI                    */
+} tv_status;
+
+/* Reference Vertex (tet_grid.hpp:41-49): fixed point, position = q / 2^24. */
+typedef struct {
+    uint32_t q[3];
+} tv_vertex;
+
+/* Byte-identical to the reference `Tet` (tet_grid.hpp:64-75; 68 bytes), so
+ * `grid.tets().data()` can be passed without conversion. */
+typedef struct {
+    uint32_t verts[4];
+    uint32_t children[2];
+    uint32_t parent;
+    uint32_t neighbors[4];
+    uint8_t normal_ids[4];
+    uint8_t level;
+    uint8_t pad0[3];
+    float density, temperature, albedo; /* MediaPayload (tet_grid.hpp:53-62) */
+    uint8_t mask;
+    uint8_t pad1[3];
+} tv_tet;
+
+/* PinholeCamera constructor arguments (camera.hpp:18-19). The basis, tan and
+ * frustum planes are derived on the host exactly as camera.cpp:12-45 does. */
+typedef struct {
+    double position[3];
+    double forward[3];
+    double up[3];
+    double vfov_degrees;
+    int32_t width, height;
+} tv_camera;
+
+/* RenderConfig (tracer.hpp:16-28). exposure/gamma only affect 8-bit output. */
+typedef struct {
+    int32_t spp;
+    int32_t max_bounces;
+    uint64_t seed;
+    double hg_g;
+    double default_albedo;
+    double environment[3];
+    double emission_scale;
+    double exposure;
+    double gamma;
+} tv_render_config;
+
+/* BuildConfig (builder.hpp:21-29). */
+typedef struct {
+    double variation_threshold;
+    int32_t max_level;
+    int32_t use_camera;
+    double pixel_threshold;
+    double density_scale;
+} tv_build_config;
+
+/* BuildStats (builder.hpp:31-38) plus GPU round counters. */
+typedef struct {
+    uint64_t leaf_count;
+    int32_t max_depth;
+    int32_t rounds;           /* criterion rounds                       */
+    double seconds;           /* device time of the build               */
+    uint64_t criterion_splits;
+    uint64_t propagation_splits;
+    uint64_t closure_passes;  /* bisect passes summed over all rounds   */
+    uint64_t voxel_visits;    /* sum over evaluated tets of owned voxels */
+} tv_build_stats;
+
+/* ImageAccumulator counters (image.hpp:23-26) plus device timing. */
+typedef struct {
+    uint64_t cells_visited;
+    uint64_t paths_traced;
+    uint64_t degenerate_paths;
+    double seconds;           /* device time of the render kernel(s) */
+} tv_render_stats;
+
+/* ImageAccumulator buffers (image.hpp:21-23): sum, sum_sq = 3*W*H doubles in
+ * pixel-major RGB order; sample_counts = W*H. Any pointer may be NULL to skip
+ * that output. */
+typedef struct {
+    double* sum;
+    double* sum_sq;
+    uint32_t* sample_counts;
+} tv_framebuffer;
+
+/* Ray (geometry.hpp:53-60). */
+typedef struct {
+    double origin[3];
+    double dir[3];
+    double t_min, t_max;
+} tv_ray;
+
+/* RaySegment (tet_grid.hpp:82-86); cell is the reference TetId. */
+typedef struct {
+    uint32_t cell;
+    uint32_t pad;
+    double t_enter, t_exit;
+} tv_segment;
+
+typedef struct tv_grid tv_grid;
+
+typedef struct {
+    uint64_t n_vertices;
+    uint64_t n_tets;
+    uint64_t n_leaves;
+    uint64_t n_internal;
+    int32_t max_level;
+    int32_t max_depth;
+    int32_t device;
+    int32_t pad;
+    uint64_t device_bytes;
+} tv_grid_info;
+
+const char* tv_last_error(void);
+const char* tv_version(void);
+int tv_device_count(int* out);
+
+/* -- grid lifetime -------------------------------------------------------- */
+int tv_grid_upload(const tv_vertex* vertices, uint64_t n_vertices, const tv_tet* tets, uint64_t n_tets,
+                   const uint32_t roots[24], int32_t max_level, int device, tv_grid** out);
+/* Copies the pools back (reference layout, reference TetIds). Query sizes
+ * with tv_grid_get_info; any output pointer may be NULL. */
+int tv_grid_download(const tv_grid* g, tv_vertex* vertices, tv_tet* tets, uint32_t roots[24]);
+int tv_grid_get_info(const tv_grid* g, tv_grid_info* out);
+void tv_grid_free(tv_grid* g);
+
+/* -- LEB build on the GPU --------------------------------------------------- */
+/* density/temperature/albedo: nx*ny*nz floats, x fastest (volume.hpp:41-43);
+ * temperature/albedo may be NULL. camera may be NULL unless use_camera. */
+int tv_build(const float* density, const float* temperature, const float* albedo, int32_t nx, int32_t ny,
+             int32_t nz, const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out,
+             tv_build_stats* stats);
+/* Same, with the density already resident on the device (float, x fastest). */
+int tv_build_dev(const float* density_dev, const float* temperature_dev, const float* albedo_dev, int32_t nx,
+                 int32_t ny, int32_t nz, const tv_build_config* cfg, const tv_camera* camera, int device,
+                 tv_grid** out, tv_build_stats* stats);
+/* Procedural fields on the device (kind: 0 constant, 1 ramp, 2 blob, 3 step,
+ * 4 noise, 5 cloud; cli.cpp:317-346). out_dev: nx*ny*nz f32. */
+int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, double value, float* out_dev,
+                           int device);
+
+/* -- render ------------------------------------------------------------------ */
+int tv_render(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg, tv_framebuffer* out,
+              tv_render_stats* stats);
+/* Multi-GPU share: renders the interleaved 16x16 tiles t with
+ * t % n_ranks == rank (tile t = row-major over ceil(W/16) x ceil(H/16)).
+ * Outputs are DEVICE pointers to full-frame buffers (only this rank's pixels
+ * are written) and the call is asynchronous on `stream`; stats_dev (3 u64:
+ * cells_visited, paths_traced, degenerate_paths) is accumulated atomically. */
+int tv_render_tiles(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg, int32_t rank,
+                    int32_t n_ranks, double* sum_dev, double* sum_sq_dev, uint32_t* counts_dev, uint64_t* stats_dev,
+                    void* stream);
+/* Packs this rank's tiles of a full-frame device buffer (elem_words 64-bit
+ * words per pixel) into a contiguous buffer of tv_tile_pack_words() words
+ * (for one NCCL all-gather), and the inverse for the gathered buffers. */
+uint64_t tv_tile_pack_words(int32_t width, int32_t height, int32_t rank, int32_t n_ranks, int32_t elem_words);
+int tv_tile_pack(const void* frame_dev, void* packed_dev, int32_t width, int32_t height, int32_t rank,
+                 int32_t n_ranks, int32_t elem_words, void* stream);
+int tv_tile_unpack(const void* packed_dev, void* frame_dev, int32_t width, int32_t height, int32_t rank,
+                   int32_t n_ranks, int32_t elem_words, void* stream);
+
+/* -- parity entry points ------------------------------------------------------ */
+/* Segments of n rays. offsets has n+1 entries; at most cap segments are
+ * written; *total receives the full count. */
+int tv_march_segments(const tv_grid* g, const tv_ray* rays, uint64_t n, tv_segment* out, uint64_t* offsets,
+                      uint64_t cap, uint64_t* total, uint64_t* degenerate_paths);
+/* points: 3*n doubles; out: reference TetIds (TV_NO_TET when outside). */
+int tv_locate_points(const tv_grid* g, const double* points, uint64_t n, uint32_t* out);
+
+/* -- regular-grid comparator (config 5) ---------------------------------------- */
+int tv_render_regular(const float* density, int32_t nx, int32_t ny, int32_t nz, double density_scale,
+                      const tv_camera* camera, const tv_render_config* cfg, int device, tv_framebuffer* out,
+                      tv_render_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

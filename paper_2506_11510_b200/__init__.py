@@ -1,0 +1,474 @@
+"""tetvol_b200 — B200-native adaptive-tetrahedral-grid volumetric path tracer.
+
+Host-side Python mirror of the reference ``tetvol`` C++ API for the hot path
+(``render``, ``build_adaptive_grid``, ``march_segments``, ``PinholeCamera``,
+``RenderConfig``, ``BuildConfig``, ``ImageAccumulator``; see
+/root/reference/proj/include/tetvol/{tracer,builder,camera,image}.hpp), calling
+the sm_100a CUDA library ``_lib/libtetvol_b200.so`` through its C ABI
+(``include/tetvol_b200.h``). Errors map to the reference exception names.
+
+There is no CPU fallback: importing this package without the built library
+raises ImportError, and every compute call without a CUDA device raises
+``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libtetvol_b200.so")
+NO_TET = 0xFFFFFFFF
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C paper_2506_11510_b200/csrc` "
+        "(or __graft_entry__.build()); there is no CPU fallback"
+    )
+_lib = C.CDLL(LIB_PATH)
+
+
+# ---------------------------------------------------------------- errors ---
+class TetvolError(RuntimeError):
+    """Runtime failure (reference: std::runtime_error)."""
+
+
+class ConfigError(TetvolError):
+    """errors.hpp:7-9"""
+
+
+class CameraError(TetvolError):
+    """camera.hpp:10-12"""
+
+
+class GridError(TetvolError):
+    """tet_grid.hpp:24-26"""
+
+
+class OutsideGrid(GridError):
+    """tet_grid.hpp:33-35"""
+
+
+class CudaError(TetvolError):
+    """No usable CUDA device, or a launch/copy failed."""
+
+
+_ERRS = {1: TetvolError, 2: ConfigError, 3: CameraError, 4: GridError, 5: OutsideGrid, 6: CudaError,
+         7: CudaError, 8: ValueError}
+
+
+def _check(rc: int):
+    if rc:
+        msg = _lib.tv_last_error().decode()
+        raise _ERRS.get(rc, TetvolError)(msg)
+
+
+# ------------------------------------------------------------- C structs ---
+class _Camera(C.Structure):
+    _fields_ = [("position", C.c_double * 3), ("forward", C.c_double * 3), ("up", C.c_double * 3),
+                ("vfov_degrees", C.c_double), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class _RenderConfig(C.Structure):
+    _fields_ = [("spp", C.c_int32), ("max_bounces", C.c_int32), ("seed", C.c_uint64), ("hg_g", C.c_double),
+                ("default_albedo", C.c_double), ("environment", C.c_double * 3), ("emission_scale", C.c_double),
+                ("exposure", C.c_double), ("gamma", C.c_double)]
+
+
+class _BuildConfig(C.Structure):
+    _fields_ = [("variation_threshold", C.c_double), ("max_level", C.c_int32), ("use_camera", C.c_int32),
+                ("pixel_threshold", C.c_double), ("density_scale", C.c_double)]
+
+
+class _BuildStats(C.Structure):
+    _fields_ = [("leaf_count", C.c_uint64), ("max_depth", C.c_int32), ("rounds", C.c_int32),
+                ("seconds", C.c_double), ("criterion_splits", C.c_uint64), ("propagation_splits", C.c_uint64),
+                ("closure_passes", C.c_uint64), ("voxel_visits", C.c_uint64)]
+
+
+class _RenderStats(C.Structure):
+    _fields_ = [("cells_visited", C.c_uint64), ("paths_traced", C.c_uint64), ("degenerate_paths", C.c_uint64),
+                ("seconds", C.c_double)]
+
+
+class _Framebuffer(C.Structure):
+    _fields_ = [("sum", C.POINTER(C.c_double)), ("sum_sq", C.POINTER(C.c_double)),
+                ("sample_counts", C.POINTER(C.c_uint32))]
+
+
+class _GridInfo(C.Structure):
+    _fields_ = [("n_vertices", C.c_uint64), ("n_tets", C.c_uint64), ("n_leaves", C.c_uint64),
+                ("n_internal", C.c_uint64), ("max_level", C.c_int32), ("max_depth", C.c_int32),
+                ("device", C.c_int32), ("pad", C.c_int32), ("device_bytes", C.c_uint64)]
+
+
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_F = C.POINTER(C.c_float)
+_U32 = C.POINTER(C.c_uint32)
+_U64 = C.POINTER(C.c_uint64)
+
+
+def _sig(name, res, *args):
+    fn = getattr(_lib, name)
+    fn.restype = res
+    fn.argtypes = list(args)
+    return fn
+
+
+_sig("tv_last_error", C.c_char_p)
+_sig("tv_version", C.c_char_p)
+_sig("tv_device_count", C.c_int, C.POINTER(C.c_int))
+_sig("tv_grid_upload", C.c_int, _P, C.c_uint64, _P, C.c_uint64, _U32, C.c_int32, C.c_int, C.POINTER(_P))
+_sig("tv_grid_download", C.c_int, _P, _P, _P, _U32)
+_sig("tv_grid_get_info", C.c_int, _P, C.POINTER(_GridInfo))
+_sig("tv_grid_free", None, _P)
+_sig("tv_build", C.c_int, _F, _F, _F, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_BuildConfig), C.POINTER(_Camera),
+     C.c_int, C.POINTER(_P), C.POINTER(_BuildStats))
+_sig("tv_build_dev", C.c_int, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_BuildConfig),
+     C.POINTER(_Camera), C.c_int, C.POINTER(_P), C.POINTER(_BuildStats))
+_sig("tv_generate_volume_dev", C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, C.c_int)
+_sig("tv_render", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.POINTER(_Framebuffer),
+     C.POINTER(_RenderStats))
+_sig("tv_render_tiles", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.c_int32, C.c_int32, _P, _P, _P,
+     _P, _P)
+_sig("tv_tile_pack_words", C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32)
+_sig("tv_tile_pack", C.c_int, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P)
+_sig("tv_tile_unpack", C.c_int, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P)
+_sig("tv_march_segments", C.c_int, _P, _P, C.c_uint64, _P, _U64, C.c_uint64, _U64, _U64)
+_sig("tv_locate_points", C.c_int, _P, _D, C.c_uint64, _U32)
+_sig("tv_render_regular", C.c_int, _F, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
+     C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
+
+# reference Tet layout (tet_grid.hpp:64-75; 68 bytes)
+TET_DTYPE = np.dtype([("verts", "<u4", 4), ("children", "<u4", 2), ("parent", "<u4"), ("neighbors", "<u4", 4),
+                      ("normal_ids", "u1", 4), ("level", "u1"), ("pad0", "u1", 3), ("density", "<f4"),
+                      ("temperature", "<f4"), ("albedo", "<f4"), ("mask", "u1"), ("pad1", "u1", 3)])
+SEGMENT_DTYPE = np.dtype([("cell", "<u4"), ("pad", "<u4"), ("t_enter", "<f8"), ("t_exit", "<f8")])
+
+
+def version() -> str:
+    return _lib.tv_version().decode()
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(_lib.tv_device_count(C.byref(n)))
+    return n.value
+
+
+# ------------------------------------------------------ config mirrors ---
+@dataclass
+class PinholeCamera:
+    """camera.hpp:16-48 (validated by the library exactly as camera.cpp:15-20)."""
+
+    position: tuple = (0.5, 0.5, -2.0)
+    forward: tuple = (0.0, 0.0, 1.0)
+    up: tuple = (0.0, 1.0, 0.0)
+    vfov_degrees: float = 40.0
+    width: int = 256
+    height: int = 256
+
+    def _c(self) -> _Camera:
+        c = _Camera()
+        c.position[:] = [float(x) for x in self.position]
+        c.forward[:] = [float(x) for x in self.forward]
+        c.up[:] = [float(x) for x in self.up]
+        c.vfov_degrees = float(self.vfov_degrees)
+        c.width, c.height = int(self.width), int(self.height)
+        return c
+
+
+@dataclass
+class RenderConfig:
+    """tracer.hpp:16-28"""
+
+    spp: int = 32
+    max_bounces: int = 64
+    seed: int = 0
+    hg_g: float = 0.0
+    default_albedo: float = 0.8
+    environment: tuple = (1.0, 1.0, 1.0)
+    emission_scale: float = 1.0
+    exposure: float = 1.0
+    gamma: float = 2.2
+
+    def _c(self) -> _RenderConfig:
+        r = _RenderConfig()
+        r.spp, r.max_bounces, r.seed = int(self.spp), int(self.max_bounces), int(self.seed)
+        r.hg_g, r.default_albedo = float(self.hg_g), float(self.default_albedo)
+        r.environment[:] = [float(x) for x in self.environment]
+        r.emission_scale, r.exposure, r.gamma = float(self.emission_scale), float(self.exposure), float(self.gamma)
+        return r
+
+
+@dataclass
+class BuildConfig:
+    """builder.hpp:21-29"""
+
+    variation_threshold: float = 0.1
+    max_level: int = 24
+    use_camera: bool = False
+    pixel_threshold: float = 1.0
+    density_scale: float = 1.0
+
+    def _c(self) -> _BuildConfig:
+        b = _BuildConfig()
+        b.variation_threshold, b.max_level, b.use_camera = float(self.variation_threshold), int(self.max_level), int(
+            bool(self.use_camera))
+        b.pixel_threshold, b.density_scale = float(self.pixel_threshold), float(self.density_scale)
+        return b
+
+
+@dataclass
+class BuildStats:
+    """builder.hpp:31-38 plus GPU round counters."""
+
+    leaf_count: int = 0
+    max_depth: int = 0
+    rounds: int = 0
+    seconds: float = 0.0
+    criterion_splits: int = 0
+    propagation_splits: int = 0
+    closure_passes: int = 0
+    voxel_visits: int = 0
+
+
+@dataclass
+class ImageAccumulator:
+    """image.hpp:18-70 (host copy of the framebuffer)."""
+
+    width: int
+    height: int
+    sum: np.ndarray
+    sum_sq: np.ndarray
+    sample_counts: np.ndarray
+    cells_visited: int = 0
+    paths_traced: int = 0
+    degenerate_paths: int = 0
+    seconds: float = 0.0
+
+    def mean(self) -> np.ndarray:
+        n = self.sample_counts.reshape(-1, 1).astype(np.float64)
+        m = np.zeros_like(self.sum.reshape(-1, 3))
+        nz = n[:, 0] > 0
+        m[nz] = self.sum.reshape(-1, 3)[nz] / n[nz]
+        return m.reshape(self.height, self.width, 3)
+
+    def variance_of_mean(self) -> np.ndarray:
+        """image.hpp:56-69"""
+        n = self.sample_counts.reshape(-1, 1).astype(np.float64)
+        s = self.sum.reshape(-1, 3)
+        q = self.sum_sq.reshape(-1, 3)
+        out = np.zeros_like(s)
+        ok = n[:, 0] >= 2
+        m = s[ok] / n[ok]
+        var = (q[ok] - n[ok] * m * m) / (n[ok] - 1.0)
+        out[ok] = np.maximum(0.0, var) / n[ok]
+        return out.reshape(self.height, self.width, 3)
+
+
+# ------------------------------------------------------------------ grid ---
+class TetGrid:
+    """A tet grid resident in one GPU's HBM (opaque ``tv_grid`` handle)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def upload(cls, vertices: np.ndarray, tets: np.ndarray, roots, max_level: int = 48, device: int = 0):
+        """From reference pools: vertices (nv,3) u32 fixed point, tets (nt,) TET_DTYPE, roots (24,) u32."""
+        v = np.ascontiguousarray(vertices, np.uint32)
+        t = np.ascontiguousarray(tets)
+        if t.dtype != TET_DTYPE:
+            raise ValueError("tets must use TET_DTYPE (the reference 68-byte Tet layout)")
+        r = np.ascontiguousarray(roots, np.uint32)
+        if r.shape != (24,):
+            raise ValueError("roots must have 24 entries")
+        h = _P()
+        _check(_lib.tv_grid_upload(v.ctypes.data_as(_P), len(v), t.ctypes.data_as(_P), len(t), r.ctypes.data_as(_U32),
+                                   int(max_level), int(device), C.byref(h)))
+        return cls(h)
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise ValueError("grid is closed")
+        return self._h
+
+    def info(self) -> dict:
+        gi = _GridInfo()
+        _check(_lib.tv_grid_get_info(self.handle, C.byref(gi)))
+        return {k: getattr(gi, k) for k, _ in _GridInfo._fields_ if k != "pad"}
+
+    def download(self):
+        """-> (vertices (nv,3) u32, tets (nt,) TET_DTYPE, roots (24,) u32) in reference layout and ids."""
+        i = self.info()
+        v = np.zeros((i["n_vertices"], 3), np.uint32)
+        t = np.zeros(i["n_tets"], TET_DTYPE)
+        r = np.zeros(24, np.uint32)
+        _check(_lib.tv_grid_download(self.handle, v.ctypes.data_as(_P), t.ctypes.data_as(_P), r.ctypes.data_as(_U32)))
+        return v, t, r
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.tv_grid_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# ---------------------------------------------------------------- calls ---
+def render(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, threads: int = 0) -> ImageAccumulator:
+    """tracer.hpp:84-85. ``threads`` is accepted for signature parity and ignored."""
+    del threads
+    w, h = int(camera.width), int(camera.height)
+    s = np.zeros(w * h * 3)
+    sq = np.zeros(w * h * 3)
+    cnt = np.zeros(w * h, np.uint32)
+    fb = _Framebuffer(s.ctypes.data_as(_D), sq.ctypes.data_as(_D), cnt.ctypes.data_as(_U32))
+    st = _RenderStats()
+    cam, rc = camera._c(), cfg._c()
+    _check(_lib.tv_render(grid.handle, C.byref(cam), C.byref(rc), C.byref(fb), C.byref(st)))
+    return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
+
+
+def render_into(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, sum_out: np.ndarray,
+                sum_sq_out: np.ndarray | None = None, counts_out: np.ndarray | None = None) -> dict:
+    """render() into caller-provided (e.g. pinned) host buffers; returns the stats."""
+    fb = _Framebuffer(sum_out.ctypes.data_as(_D), None if sum_sq_out is None else sum_sq_out.ctypes.data_as(_D),
+                      None if counts_out is None else counts_out.ctypes.data_as(_U32))
+    st = _RenderStats()
+    cam, rc = camera._c(), cfg._c()
+    _check(_lib.tv_render(grid.handle, C.byref(cam), C.byref(rc), C.byref(fb), C.byref(st)))
+    return dict(cells_visited=st.cells_visited, paths_traced=st.paths_traced, degenerate_paths=st.degenerate_paths,
+                seconds=st.seconds)
+
+
+def render_tiles(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, rank: int, n_ranks: int, sum_dev: int,
+                 sum_sq_dev: int | None, counts_dev: int | None, stats_dev: int | None, stream: int = 0):
+    """Asynchronous per-rank share of a frame into device buffers (raw device pointers)."""
+    cam, rc = camera._c(), cfg._c()
+    _check(_lib.tv_render_tiles(grid.handle, C.byref(cam), C.byref(rc), int(rank), int(n_ranks), sum_dev, sum_sq_dev,
+                                counts_dev, stats_dev, stream))
+
+
+def tile_pack_words(width: int, height: int, rank: int, n_ranks: int, elem_words: int) -> int:
+    return int(_lib.tv_tile_pack_words(width, height, rank, n_ranks, elem_words))
+
+
+def tile_pack(frame_dev: int, packed_dev: int, width, height, rank, n_ranks, elem_words, stream: int = 0):
+    _check(_lib.tv_tile_pack(frame_dev, packed_dev, width, height, rank, n_ranks, elem_words, stream))
+
+
+def tile_unpack(packed_dev: int, frame_dev: int, width, height, rank, n_ranks, elem_words, stream: int = 0):
+    _check(_lib.tv_tile_unpack(packed_dev, frame_dev, width, height, rank, n_ranks, elem_words, stream))
+
+
+def march_segments(grid: TetGrid, rays: np.ndarray):
+    """tracer.hpp:49 over a batch. rays: (n, 8) [origin, dir, t_min, t_max].
+
+    Returns (segments: SEGMENT_DTYPE array, offsets: (n+1,) u64, degenerate_paths)."""
+    r = np.ascontiguousarray(rays, np.float64)
+    if r.ndim != 2 or r.shape[1] != 8:
+        raise ValueError("rays must be (n, 8)")
+    n = len(r)
+    off = np.zeros(n + 1, np.uint64)
+    total = C.c_uint64()
+    deg = C.c_uint64()
+    _check(_lib.tv_march_segments(grid.handle, r.ctypes.data_as(_P), n, None, off.ctypes.data_as(_U64), 0,
+                                  C.byref(total), C.byref(deg)))
+    seg = np.zeros(total.value, SEGMENT_DTYPE)
+    _check(_lib.tv_march_segments(grid.handle, r.ctypes.data_as(_P), n, seg.ctypes.data_as(_P),
+                                  off.ctypes.data_as(_U64), total.value, C.byref(total), C.byref(deg)))
+    return seg, off, deg.value
+
+
+def locate_points(grid: TetGrid, points: np.ndarray) -> np.ndarray:
+    """TetGrid::locate_point over a batch (tet_grid.hpp:166); NO_TET outside the cube."""
+    p = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    out = np.zeros(len(p), np.uint32)
+    _check(_lib.tv_locate_points(grid.handle, p.ctypes.data_as(_D), len(p), out.ctypes.data_as(_U32)))
+    return out
+
+
+def _vol_ptrs(volume, temperature=None, albedo=None):
+    v = np.ascontiguousarray(volume, np.float32)
+    if v.ndim != 3:
+        raise ValueError("volume must be (nz, ny, nx) float32, x fastest")
+    t = None if temperature is None else np.ascontiguousarray(temperature, np.float32)
+    a = None if albedo is None else np.ascontiguousarray(albedo, np.float32)
+    return v, t, a
+
+
+def build_adaptive_grid(volume: np.ndarray, cfg: BuildConfig, camera: PinholeCamera | None = None,
+                        temperature: np.ndarray | None = None, albedo: np.ndarray | None = None,
+                        device: int = 0):
+    """builder.hpp:51-52 on the GPU. volume: (nz, ny, nx) float32 density. -> (TetGrid, BuildStats)."""
+    v, t, a = _vol_ptrs(volume, temperature, albedo)
+    nz, ny, nx = v.shape
+    h = _P()
+    st = _BuildStats()
+    bc = cfg._c()
+    cam = camera._c() if camera is not None else None
+    _check(_lib.tv_build(v.ctypes.data_as(_F), None if t is None else t.ctypes.data_as(_F),
+                         None if a is None else a.ctypes.data_as(_F), nx, ny, nz, C.byref(bc),
+                         C.byref(cam) if cam is not None else None, int(device), C.byref(h), C.byref(st)))
+    return TetGrid(h), BuildStats(**{k: getattr(st, k) for k, _ in _BuildStats._fields_})
+
+
+def build_adaptive_grid_dev(density_dev: int, shape, cfg: BuildConfig, camera: PinholeCamera | None = None,
+                            device: int = 0, temperature_dev: int | None = None, albedo_dev: int | None = None):
+    """Same, with the density already in HBM (raw device pointer; shape = (nz, ny, nx))."""
+    nz, ny, nx = shape
+    h = _P()
+    st = _BuildStats()
+    bc = cfg._c()
+    cam = camera._c() if camera is not None else None
+    _check(_lib.tv_build_dev(density_dev, temperature_dev, albedo_dev, nx, ny, nz, C.byref(bc),
+                             C.byref(cam) if cam is not None else None, int(device), C.byref(h), C.byref(st)))
+    return TetGrid(h), BuildStats(**{k: getattr(st, k) for k, _ in _BuildStats._fields_})
+
+
+VOLUME_KINDS = {"constant": 0, "ramp": 1, "blob": 2, "step": 3, "noise": 4, "cloud": 5}
+
+
+def generate_volume_dev(kind: str, n: int, out_dev: int, device: int = 0, value: float = 1.0):
+    """Procedural density field written into HBM (n^3 float32 at out_dev)."""
+    _check(_lib.tv_generate_volume_dev(VOLUME_KINDS[kind], n, n, n, float(value), out_dev, int(device)))
+
+
+def render_reference(volume: np.ndarray, density_scale: float, camera: PinholeCamera, cfg: RenderConfig,
+                     device: int = 0) -> ImageAccumulator:
+    """regular_grid.hpp:66-67: RegularGrid::from_volume + render_reference on the GPU."""
+    v, _, _ = _vol_ptrs(volume)
+    nz, ny, nx = v.shape
+    w, h = int(camera.width), int(camera.height)
+    s = np.zeros(w * h * 3)
+    sq = np.zeros(w * h * 3)
+    cnt = np.zeros(w * h, np.uint32)
+    fb = _Framebuffer(s.ctypes.data_as(_D), sq.ctypes.data_as(_D), cnt.ctypes.data_as(_U32))
+    st = _RenderStats()
+    cam, rc = camera._c(), cfg._c()
+    _check(_lib.tv_render_regular(v.ctypes.data_as(_F), nx, ny, nz, float(density_scale), C.byref(cam), C.byref(rc),
+                                  int(device), C.byref(fb), C.byref(st)))
+    return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
+
+
+__all__ = [
+    "BuildConfig", "BuildStats", "CameraError", "ConfigError", "CudaError", "GridError", "ImageAccumulator",
+    "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
+    "build_adaptive_grid", "build_adaptive_grid_dev", "device_count", "generate_volume_dev", "locate_points",
+    "march_segments", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",
+    "tile_unpack", "version",
+]

@@ -1,0 +1,439 @@
+// C ABI of tetvol_b200 (include/tetvol_b200.h). Host-side mirror of the
+// reference API: argument validation with the reference's rules and messages,
+// the pinhole camera precompute, device memory management and kernel launches.
+// No exception crosses this boundary.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tv_trace.cuh"
+
+namespace tvb {
+
+namespace {
+thread_local std::string g_err;
+}
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return TV_OK;
+    if (e == cudaErrorMemoryAllocation)
+        return set_error(TV_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+    return set_error(TV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+#define TV_CK(x, what)                                  \
+    do {                                                \
+        int rc_ = cuda_status((x), what);               \
+        if (rc_) return rc_;                            \
+    } while (0)
+
+// camera.cpp:12-45 (host; std::tan runs here, never on the device)
+int make_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]) {
+    if (!c) return set_error(TV_ERR_ARG, "camera is null");
+    if (c->width < 1 || c->height < 1) return set_error(TV_ERR_CAMERA, "image dimensions must be positive");
+    if (!(c->vfov_degrees > 0.0 && c->vfov_degrees < 180.0))
+        return set_error(TV_ERR_CAMERA, "vfov must be in (0, 180) degrees");
+    const d3 f = mk(c->forward[0], c->forward[1], c->forward[2]);
+    const d3 up = mk(c->up[0], c->up[1], c->up[2]);
+    if (std::sqrt(dot(f, f)) == 0.0) return set_error(TV_ERR_CAMERA, "forward vector must be nonzero");
+    const d3 fwd = normalize(f);
+    const d3 upo = sub(up, mul(fwd, dot(up, fwd)));
+    if (std::sqrt(dot(upo, upo)) < 1e-12) return set_error(TV_ERR_CAMERA, "up vector is parallel to the view direction");
+    const d3 upn = normalize(upo);
+    const d3 right = cross(upn, fwd);
+    const double kPi = 3.14159265358979323846;
+    v.pos[0] = c->position[0], v.pos[1] = c->position[1], v.pos[2] = c->position[2];
+    v.fwd[0] = fwd.x, v.fwd[1] = fwd.y, v.fwd[2] = fwd.z;
+    v.up[0] = upn.x, v.up[1] = upn.y, v.up[2] = upn.z;
+    v.right[0] = right.x, v.right[1] = right.y, v.right[2] = right.z;
+    v.tan_half = std::tan(c->vfov_degrees * kPi / 360.0);
+    v.aspect = static_cast<double>(c->width) / c->height;
+    v.w = c->width;
+    v.h = c->height;
+    if (pn) {
+        auto corner = [&](double u, double vv) {
+            return normalize(add(add(fwd, mul(right, (2.0 * u - 1.0) * v.tan_half * v.aspect)),
+                                 mul(upn, (1.0 - 2.0 * vv) * v.tan_half)));
+        };
+        const d3 tl = corner(0, 0), tr = corner(1, 0), bl = corner(0, 1), br = corner(1, 1);
+        const d3 pos = mk(v.pos[0], v.pos[1], v.pos[2]);
+        pn[0] = fwd;
+        pd[0] = dot(fwd, pos) + 1e-4;
+        const d3 pairs[4][2] = {{tl, bl}, {br, tr}, {tr, tl}, {bl, br}};
+        for (int i = 0; i < 4; ++i) {
+            d3 n = normalize(cross(pairs[i][0], pairs[i][1]));
+            if (dot(n, fwd) < 0.0) n = mk(-n.x, -n.y, -n.z);
+            pn[i + 1] = n;
+            pd[i + 1] = dot(n, pos);
+        }
+    }
+    return TV_OK;
+}
+
+// RenderConfig::validate (tracer.cpp:131-141)
+int validate_render(const tv_render_config* r) {
+    if (!r) return set_error(TV_ERR_ARG, "render config is null");
+    if (r->spp < 1) return set_error(TV_ERR_CONFIG, "spp must be at least 1");
+    if (r->max_bounces < 1) return set_error(TV_ERR_CONFIG, "maxBounces must be at least 1");
+    if (!(r->hg_g > -1.0 && r->hg_g < 1.0)) return set_error(TV_ERR_CONFIG, "phase anisotropy g must be in (-1, 1)");
+    if (!(r->default_albedo >= 0.0 && r->default_albedo <= 1.0))
+        return set_error(TV_ERR_CONFIG, "albedo must be in [0, 1]");
+    if (r->environment[0] < 0.0 || r->environment[1] < 0.0 || r->environment[2] < 0.0)
+        return set_error(TV_ERR_CONFIG, "environment radiance must be non-negative");
+    if (r->emission_scale < 0.0) return set_error(TV_ERR_CONFIG, "emissionScale must be non-negative");
+    if (!(r->exposure > 0.0)) return set_error(TV_ERR_CONFIG, "exposure must be positive");
+    if (!(r->gamma > 0.0)) return set_error(TV_ERR_CONFIG, "gamma must be positive");
+    return TV_OK;
+}
+
+RenderParams make_params(const tv_render_config* r) {
+    RenderParams p;
+    p.spp = r->spp;
+    p.max_bounces = r->max_bounces;
+    p.seed = r->seed;
+    p.g = r->hg_g;
+    p.default_albedo = r->default_albedo;
+    p.env[0] = r->environment[0], p.env[1] = r->environment[1], p.env[2] = r->environment[2];
+    p.emission_scale = r->emission_scale;
+    return p;
+}
+
+int use_device(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return set_error(TV_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) return set_error(TV_ERR_CUDA, "device index out of range");
+    return cuda_status(cudaSetDevice(device), "cudaSetDevice");
+}
+
+int render_blocks(int device) {
+    static std::mutex mu;
+    static int cached[64] = {0};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel, kRenderThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int b = sms * per_sm;
+    if (device >= 0 && device < 64) cached[device] = b;
+    return b;
+}
+
+// Launches the persistent render kernel over this rank's tiles.
+int launch_render(const DeviceGrid& g, const CamView& cv, const RenderParams& rp, int rank, int n_ranks,
+                  RenderOut out, uint32_t* counter, cudaStream_t st) {
+    const uint32_t tiles_x = (static_cast<uint32_t>(cv.w) + 15) / 16;
+    const uint32_t tiles_y = (static_cast<uint32_t>(cv.h) + 15) / 16;
+    const uint64_t tiles = static_cast<uint64_t>(tiles_x) * tiles_y;
+    const uint64_t mine = tiles > static_cast<uint64_t>(rank) ? (tiles - rank + n_ranks - 1) / n_ranks : 0;
+    TileSched S;
+    S.counter = counter;
+    S.n_units = static_cast<uint32_t>(mine * 8);
+    S.tiles_x = tiles_x;
+    S.rank = rank;
+    S.n_ranks = n_ranks;
+    TV_CK(cudaMemsetAsync(counter, 0, sizeof(uint32_t), st), "memset counter");
+    const int nb = render_blocks(g.device);
+    const uint64_t need = (S.n_units + (kRenderThreads / 32) - 1) / (kRenderThreads / 32);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nb, std::max<uint64_t>(need, 1)));
+    render_kernel<<<grid, kRenderThreads, 0, st>>>(g.view, cv, rp, S, out);
+    return cuda_status(cudaGetLastError(), "render_kernel launch");
+}
+
+// Per-device scratch reused across tv_render calls (avoids cudaMalloc in the
+// per-frame path).
+struct Scratch {
+    int device = -1;
+    size_t bytes = 0;
+    void* buf = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+std::mutex g_scratch_mu;
+Scratch g_scratch[64];
+
+int scratch_for(int device, size_t bytes, Scratch*& out) {
+    if (device < 0 || device >= 64) return set_error(TV_ERR_ARG, "device index out of range");
+    Scratch& s = g_scratch[device];
+    if (!s.stream) {
+        TV_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream create");
+        TV_CK(cudaEventCreate(&s.ev0), "event create");
+        TV_CK(cudaEventCreate(&s.ev1), "event create");
+    }
+    if (s.bytes < bytes) {
+        cudaFree(s.buf);
+        s.buf = nullptr;
+        s.bytes = 0;
+        TV_CK(cudaMalloc(&s.buf, bytes), "scratch alloc");
+        s.bytes = bytes;
+    }
+    s.device = device;
+    out = &s;
+    return TV_OK;
+}
+
+}  // namespace
+}  // namespace tvb
+
+using namespace tvb;
+
+extern "C" {
+
+const char* tv_last_error(void) { return g_err.c_str(); }
+const char* tv_version(void) { return "tetvol_b200 0.1 (sm_100a)"; }
+
+int tv_device_count(int* out) {
+    if (!out) return set_error(TV_ERR_ARG, "out is null");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    *out = e == cudaSuccess ? n : 0;
+    return TV_OK;
+}
+
+int tv_grid_upload(const tv_vertex* vertices, uint64_t n_vertices, const tv_tet* tets, uint64_t n_tets,
+                   const uint32_t roots[24], int32_t max_level, int device, tv_grid** out) {
+    if (!vertices || !tets || !roots || !out) return set_error(TV_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (n_tets < 24 || n_tets >= (1ull << 31)) return set_error(TV_ERR_GRID, "bad tet count");
+    if (n_vertices < 8 || n_vertices > (1ull << 32)) return set_error(TV_ERR_GRID, "bad vertex count");
+    if (max_level < 1 || max_level > 48) return set_error(TV_ERR_GRID, "max_level out of range");
+    // Structural checks the kernels rely on (the reference's load_grid makes
+    // the same range checks, builder.cpp:253-285).
+    uint64_t leaves = 0;
+    for (uint64_t t = 0; t < n_tets; ++t) {
+        const tv_tet& tt = tets[t];
+        for (int k = 0; k < 4; ++k) {
+            if (tt.verts[k] >= n_vertices) return set_error(TV_ERR_GRID, "vertex id out of range");
+            if (tt.neighbors[k] != TV_NO_TET && tt.neighbors[k] >= n_tets)
+                return set_error(TV_ERR_GRID, "neighbor id out of range");
+            if (tt.normal_ids[k] >= 18) return set_error(TV_ERR_GRID, "face normal id out of range");
+        }
+        const bool leaf = tt.children[0] == TV_NO_TET;
+        if (!leaf && (tt.children[0] >= n_tets || tt.children[1] >= n_tets))
+            return set_error(TV_ERR_GRID, "child id out of range");
+        leaves += leaf;
+    }
+    for (int r = 0; r < 24; ++r)
+        if (roots[r] >= n_tets) return set_error(TV_ERR_GRID, "root id out of range");
+    int rc = use_device(device);
+    if (rc) return rc;
+
+    auto h = std::make_unique<tv_grid>();
+    DeviceGrid& g = h->g;
+    g.device = device;
+    g.n_vertices = n_vertices;
+    g.n_tets = n_tets;
+    g.n_leaves = leaves;
+    g.n_internal = n_tets - leaves;
+    g.max_level = max_level;
+    std::memcpy(g.roots, roots, sizeof(g.roots));
+    std::vector<uint4> vq(n_vertices);
+    for (uint64_t i = 0; i < n_vertices; ++i) vq[i] = make_uint4(vertices[i].q[0], vertices[i].q[1], vertices[i].q[2], 0);
+    cudaError_t e = cudaMalloc(&g.verts, n_vertices * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMalloc(&g.tets, n_tets * sizeof(tv_tet));
+    if (e != cudaSuccess) {
+        free_grid(g);
+        return cuda_status(e, "grid alloc");
+    }
+    g.bytes = n_vertices * sizeof(uint4) + n_tets * sizeof(tv_tet);
+    e = cudaMemcpy(g.verts, vq.data(), n_vertices * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g.tets, tets, n_tets * sizeof(tv_tet), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        free_grid(g);
+        return cuda_status(e, "grid upload");
+    }
+    rc = finalize_grid(g, nullptr);
+    if (rc) {
+        free_grid(g);
+        return rc;
+    }
+    *out = h.release();
+    return TV_OK;
+}
+
+int tv_grid_download(const tv_grid* h, tv_vertex* vertices, tv_tet* tets, uint32_t roots[24]) {
+    if (!h) return set_error(TV_ERR_ARG, "grid is null");
+    const DeviceGrid& g = h->g;
+    int rc = use_device(g.device);
+    if (rc) return rc;
+    if (vertices) {
+        std::vector<uint4> vq(g.n_vertices);
+        TV_CK(cudaMemcpy(vq.data(), g.verts, g.n_vertices * sizeof(uint4), cudaMemcpyDeviceToHost), "download");
+        for (uint64_t i = 0; i < g.n_vertices; ++i) {
+            vertices[i].q[0] = vq[i].x;
+            vertices[i].q[1] = vq[i].y;
+            vertices[i].q[2] = vq[i].z;
+        }
+    }
+    if (tets) TV_CK(cudaMemcpy(tets, g.tets, g.n_tets * sizeof(tv_tet), cudaMemcpyDeviceToHost), "download");
+    if (roots) std::memcpy(roots, g.roots, sizeof(g.roots));
+    return TV_OK;
+}
+
+int tv_grid_get_info(const tv_grid* h, tv_grid_info* out) {
+    if (!h || !out) return set_error(TV_ERR_ARG, "null argument");
+    const DeviceGrid& g = h->g;
+    out->n_vertices = g.n_vertices;
+    out->n_tets = g.n_tets;
+    out->n_leaves = g.n_leaves;
+    out->n_internal = g.n_internal;
+    out->max_level = g.max_level;
+    out->max_depth = g.max_depth;
+    out->device = g.device;
+    out->pad = 0;
+    out->device_bytes = g.bytes;
+    return TV_OK;
+}
+
+void tv_grid_free(tv_grid* h) {
+    if (!h) return;
+    cudaSetDevice(h->g.device);
+    free_grid(h->g);
+    delete h;
+}
+
+int tv_render(const tv_grid* h, const tv_camera* camera, const tv_render_config* cfg, tv_framebuffer* out,
+              tv_render_stats* stats) {
+    if (!h) return set_error(TV_ERR_ARG, "grid is null");
+    int rc = validate_render(cfg);
+    if (rc) return rc;
+    CamView cv;
+    if ((rc = make_camera(camera, cv, nullptr, nullptr))) return rc;
+    const DeviceGrid& g = h->g;
+    if ((rc = use_device(g.device))) return rc;
+    const uint64_t npx = static_cast<uint64_t>(cv.w) * cv.h;
+    const size_t bytes = npx * (3 * sizeof(double) * 2 + sizeof(uint32_t)) + 4 * sizeof(uint64_t) + 256;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    Scratch* s;
+    if ((rc = scratch_for(g.device, bytes, s))) return rc;
+    char* base = static_cast<char*>(s->buf);
+    double* sum = reinterpret_cast<double*>(base);
+    double* sum_sq = sum + 3 * npx;
+    uint32_t* counts = reinterpret_cast<uint32_t*>(sum_sq + 3 * npx);
+    uint64_t* st = reinterpret_cast<uint64_t*>(base + ((npx * 48 + npx * 4 + 63) & ~static_cast<size_t>(63)));
+    uint32_t* counter = reinterpret_cast<uint32_t*>(st + 3);
+    RenderOut ro{sum, sum_sq, counts, st};
+    TV_CK(cudaMemsetAsync(st, 0, 3 * sizeof(uint64_t), s->stream), "memset stats");
+    TV_CK(cudaEventRecord(s->ev0, s->stream), "event");
+    if ((rc = launch_render(g, cv, make_params(cfg), 0, 1, ro, counter, s->stream))) return rc;
+    TV_CK(cudaEventRecord(s->ev1, s->stream), "event");
+    if (out && out->sum)
+        TV_CK(cudaMemcpyAsync(out->sum, sum, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
+    if (out && out->sum_sq)
+        TV_CK(cudaMemcpyAsync(out->sum_sq, sum_sq, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost, s->stream),
+              "D2H");
+    if (out && out->sample_counts)
+        TV_CK(cudaMemcpyAsync(out->sample_counts, counts, npx * sizeof(uint32_t), cudaMemcpyDeviceToHost, s->stream),
+              "D2H");
+    uint64_t hst[3] = {0, 0, 0};
+    TV_CK(cudaMemcpyAsync(hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s->stream), "D2H");
+    TV_CK(cudaStreamSynchronize(s->stream), "render");
+    if (stats) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+        stats->cells_visited = hst[0];
+        stats->paths_traced = npx * static_cast<uint64_t>(cfg->spp);
+        stats->degenerate_paths = hst[2];
+        stats->seconds = ms * 1e-3;
+    }
+    return TV_OK;
+}
+
+int tv_render_tiles(const tv_grid* h, const tv_camera* camera, const tv_render_config* cfg, int32_t rank,
+                    int32_t n_ranks, double* sum_dev, double* sum_sq_dev, uint32_t* counts_dev, uint64_t* stats_dev,
+                    void* stream) {
+    if (!h) return set_error(TV_ERR_ARG, "grid is null");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return set_error(TV_ERR_ARG, "bad rank / n_ranks");
+    int rc = validate_render(cfg);
+    if (rc) return rc;
+    CamView cv;
+    if ((rc = make_camera(camera, cv, nullptr, nullptr))) return rc;
+    const DeviceGrid& g = h->g;
+    if ((rc = use_device(g.device))) return rc;
+    // per-(device, thread) work counter
+    thread_local uint32_t* counter[64] = {nullptr};
+    if (!counter[g.device]) TV_CK(cudaMalloc(&counter[g.device], 64), "counter alloc");
+    RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
+    return launch_render(g, cv, make_params(cfg), rank, n_ranks, ro, counter[g.device],
+                         static_cast<cudaStream_t>(stream));
+}
+
+int tv_march_segments(const tv_grid* h, const tv_ray* rays, uint64_t n, tv_segment* out, uint64_t* offsets,
+                      uint64_t cap, uint64_t* total, uint64_t* degenerate_paths) {
+    if (!h || (!rays && n)) return set_error(TV_ERR_ARG, "null argument");
+    const DeviceGrid& g = h->g;
+    int rc = use_device(g.device);
+    if (rc) return rc;
+    tv_ray* d_rays = nullptr;
+    uint64_t *d_counts = nullptr, *d_off = nullptr;
+    tv_segment* d_out = nullptr;
+    unsigned long long* d_deg = nullptr;
+    auto cleanup = [&]() { cudaFree(d_rays), cudaFree(d_counts), cudaFree(d_off), cudaFree(d_out), cudaFree(d_deg); };
+    cudaError_t e = cudaMalloc(&d_rays, (n ? n : 1) * sizeof(tv_ray));
+    if (e == cudaSuccess) e = cudaMalloc(&d_counts, (n ? n : 1) * sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d_off, (n + 1) * sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d_deg, sizeof(unsigned long long));
+    if (e == cudaSuccess && n) e = cudaMemcpy(d_rays, rays, n * sizeof(tv_ray), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(d_deg, 0, sizeof(unsigned long long));
+    const unsigned nb = static_cast<unsigned>((n + 127) / 128);
+    if (e == cudaSuccess && n) {
+        march_kernel<<<nb, 128>>>(g.view, d_rays, n, 0, d_counts, nullptr, nullptr, 0, d_deg);
+        e = cudaGetLastError();
+    }
+    std::vector<uint64_t> cnt(n), off(n + 1, 0);
+    if (e == cudaSuccess && n) e = cudaMemcpy(cnt.data(), d_counts, n * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    for (uint64_t i = 0; i < n; ++i) off[i + 1] = off[i] + cnt[i];
+    const uint64_t tot = off[n];
+    const uint64_t wcap = std::min(cap, tot);
+    if (e == cudaSuccess) e = cudaMemcpy(d_off, off.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && out && wcap) e = cudaMalloc(&d_out, wcap * sizeof(tv_segment));
+    if (e == cudaSuccess && out && wcap && n) {
+        march_kernel<<<nb, 128>>>(g.view, d_rays, n, 1, nullptr, d_off, d_out, wcap, d_deg);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && out && wcap) e = cudaMemcpy(out, d_out, wcap * sizeof(tv_segment), cudaMemcpyDeviceToHost);
+    unsigned long long deg = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&deg, d_deg, sizeof(deg), cudaMemcpyDeviceToHost);
+    cleanup();
+    if (e != cudaSuccess) return cuda_status(e, "march_segments");
+    if (offsets) std::memcpy(offsets, off.data(), (n + 1) * sizeof(uint64_t));
+    if (total) *total = tot;
+    if (degenerate_paths) *degenerate_paths = deg;
+    return TV_OK;
+}
+
+int tv_locate_points(const tv_grid* h, const double* points, uint64_t n, uint32_t* out) {
+    if (!h || ((!points || !out) && n)) return set_error(TV_ERR_ARG, "null argument");
+    if (!n) return TV_OK;
+    const DeviceGrid& g = h->g;
+    int rc = use_device(g.device);
+    if (rc) return rc;
+    double* d_p = nullptr;
+    uint32_t* d_o = nullptr;
+    cudaError_t e = cudaMalloc(&d_p, n * 3 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&d_o, n * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(d_p, points, n * 3 * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        locate_kernel<<<static_cast<unsigned>((n + 127) / 128), 128>>>(g.view, d_p, n, d_o);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(out, d_o, n * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    cudaFree(d_p);
+    cudaFree(d_o);
+    return cuda_status(e, "locate_points");
+}
+
+}  // extern "C"

@@ -1,0 +1,285 @@
+// Device grid finalize: from the reference pools (vertices, 68-byte Tet records,
+// roots) resident in HBM, build the traversal layout:
+//   * leaves renumbered along a Morton curve of their centroids (spatially
+//     adjacent leaves share cache lines; rays from neighbouring pixels hit the
+//     same lines), 64-byte LeafRec each;
+//   * internal nodes compacted to 64-byte NodeRecs with the exact bisection
+//     plane normal precomputed (tet_grid.cpp:453-470);
+//   * the 24 roots' data for the root scan (tet_grid.cpp:435-451) in the
+//     kernel parameter block.
+// The reference TetIds survive in leaf2tet (and in the kept pools), so parity
+// outputs speak reference ids.
+#include <cub/cub.cuh>
+
+#include <cstring>
+#include <vector>
+
+#include "tv_trace.cuh"
+
+namespace tvb {
+
+namespace {
+
+// slot pairs (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) (tet_grid.cpp:289)
+__host__ __device__ __forceinline__ int ep0(int e) { return e < 3 ? 0 : (e < 5 ? 1 : 2); }
+__host__ __device__ __forceinline__ int ep1(int e) { return e < 3 ? e + 1 : (e < 5 ? e - 1 : 3); }
+
+__device__ __forceinline__ uint64_t spread21(uint64_t v) {
+    v &= 0x1fffffull;
+    v = (v | v << 32) & 0x1f00000000ffffull;
+    v = (v | v << 16) & 0x1f0000ff0000ffull;
+    v = (v | v << 8) & 0x100f00f00f00f00full;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+    v = (v | v << 2) & 0x1249249249249249ull;
+    return v;
+}
+
+__global__ void keys_kernel(const tv_tet* __restrict__ tets, const uint4* __restrict__ verts, uint64_t n,
+                            uint64_t* keys, uint32_t* ids, uint32_t* is_internal) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n) return;
+    const tv_tet& tt = tets[t];
+    ids[t] = static_cast<uint32_t>(t);
+    const bool leaf = tt.children[0] == kNone;
+    is_internal[t] = leaf ? 0u : 1u;
+    if (!leaf) {
+        keys[t] = ~0ull;
+        return;
+    }
+    uint64_t c[3] = {0, 0, 0};
+    for (int k = 0; k < 4; ++k) {
+        const uint4 q = verts[tt.verts[k]];
+        c[0] += q.x, c[1] += q.y, c[2] += q.z;
+    }
+    // centroid*4 < 2^27; keep the top 21 bits per axis
+    keys[t] = spread21(c[0] >> 6) | spread21(c[1] >> 6) << 1 | spread21(c[2] >> 6) << 2;
+}
+
+__global__ void tet2leaf_kernel(const uint32_t* __restrict__ order, uint64_t n_leaves, uint32_t* tet2leaf) {
+    const uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (L < n_leaves) tet2leaf[order[L]] = static_cast<uint32_t>(L);
+}
+
+__device__ __forceinline__ uint32_t encode_child(uint32_t c, const tv_tet* tets, const uint32_t* tet2leaf,
+                                                 const uint32_t* tet2node) {
+    return tets[c].children[0] == kNone ? (kLeafBit | tet2leaf[c]) : tet2node[c];
+}
+
+__global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* __restrict__ order,
+                              const uint32_t* __restrict__ tet2leaf, uint64_t n_leaves, LeafRec* out,
+                              int* max_depth) {
+    const uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (L >= n_leaves) return;
+    const tv_tet tt = tets[order[L]];
+    LeafRec r;
+    uint32_t nid = 0;
+    for (int f = 0; f < 4; ++f) {
+        const uint32_t nb = tt.neighbors[f];
+        r.w[f] = nb == kNone ? kNone : tet2leaf[nb];
+        r.w[4 + f] = tt.verts[f];
+        uint32_t far = kNone;
+        if (nb != kNone) {
+            const tv_tet& o = tets[nb];
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t v = o.verts[j];
+                bool shared = false;
+                for (int k = 0; k < 4; ++k)
+                    if (k != f && tt.verts[k] == v) shared = true;
+                if (!shared) far = v;
+            }
+        }
+        r.w[8 + f] = far;
+        nid |= (static_cast<uint32_t>(tt.normal_ids[f]) & 31u) << (5 * f);
+    }
+    r.w[12] = nid | (static_cast<uint32_t>(tt.mask) << 20);
+    r.w[13] = __float_as_uint(tt.density);
+    r.w[14] = __float_as_uint(tt.temperature);
+    r.w[15] = __float_as_uint(tt.albedo);
+    uint4* dst = reinterpret_cast<uint4*>(out + L);
+    dst[0] = make_uint4(r.w[0], r.w[1], r.w[2], r.w[3]);
+    dst[1] = make_uint4(r.w[4], r.w[5], r.w[6], r.w[7]);
+    dst[2] = make_uint4(r.w[8], r.w[9], r.w[10], r.w[11]);
+    dst[3] = make_uint4(r.w[12], r.w[13], r.w[14], r.w[15]);
+    atomicMax(max_depth, static_cast<int>(tt.level));
+}
+
+// tet_grid.cpp:288-330 (exact integer longest edge; ties towards smaller ids)
+__device__ void refinement_slots(const tv_tet& tt, const uint4* verts, int& s0, int& s1) {
+    int best = 0;
+    uint64_t best_len = 0;
+    uint32_t bmin = 0, bmax = 0;
+    for (int e = 0; e < 6; ++e) {
+        const uint32_t a = tt.verts[ep0(e)], b = tt.verts[ep1(e)];
+        const uint4 qa = verts[a], qb = verts[b];
+        const int64_t dx = static_cast<int64_t>(qa.x) - qb.x, dy = static_cast<int64_t>(qa.y) - qb.y,
+                      dz = static_cast<int64_t>(qa.z) - qb.z;
+        const uint64_t len = static_cast<uint64_t>(dx * dx) + static_cast<uint64_t>(dy * dy) +
+                             static_cast<uint64_t>(dz * dz);
+        const uint32_t mn = a < b ? a : b, mx = a < b ? b : a;
+        bool better;
+        if (e == 0) better = true;
+        else if (len != best_len) better = len > best_len;
+        else better = mn < bmin || (mn == bmin && mx < bmax);
+        if (better) best = e, best_len = len, bmin = mn, bmax = mx;
+    }
+    s0 = ep0(best);
+    s1 = ep1(best);
+}
+
+__global__ void nodes_kernel(const tv_tet* __restrict__ tets, const uint4* __restrict__ verts, uint64_t n_tets,
+                             const uint32_t* __restrict__ tet2leaf, const uint32_t* __restrict__ tet2node,
+                             NodeRec* out) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n_tets) return;
+    const tv_tet tt = tets[t];
+    if (tt.children[0] == kNone) return;
+    int s0, s1;
+    refinement_slots(tt, verts, s0, s1);
+    const uint32_t ca = tt.children[0];
+    const d3 pm = vpos(verts[tets[ca].verts[s1]]);
+    int oa = -1, ob = -1;
+    for (int s = 0; s < 4; ++s)
+        if (s != s0 && s != s1) {
+            if (oa < 0) oa = s;
+            else ob = s;
+        }
+    const d3 pa = vpos(verts[tt.verts[oa]]), pb = vpos(verts[tt.verts[ob]]);
+    const d3 n = cross(sub(pa, pm), sub(pb, pm));
+    const double sref = dot(n, sub(vpos(verts[tt.verts[s0]]), pm));
+    NodeRec r;
+    r.n[0] = n.x, r.n[1] = n.y, r.n[2] = n.z;
+    r.pm[0] = pm.x, r.pm[1] = pm.y, r.pm[2] = pm.z;
+    r.child[0] = encode_child(ca, tets, tet2leaf, tet2node);
+    r.child[1] = encode_child(tt.children[1], tets, tet2leaf, tet2node);
+    r.sref_pos = sref > 0.0 ? 1u : 0u;
+    r.pad = 0;
+    out[tet2node[t]] = r;
+}
+
+__global__ void roots_kernel(const tv_tet* __restrict__ tets, const uint32_t* roots, const uint32_t* tet2leaf,
+                             const uint32_t* tet2node, uint32_t* out /* 24 ptr, 24 nid, 96 vid */) {
+    const int r = threadIdx.x;
+    if (r >= 24) return;
+    const tv_tet& tt = tets[roots[r]];
+    out[r] = encode_child(roots[r], tets, tet2leaf, tet2node);
+    out[24 + r] = tt.normal_ids[0] | tt.normal_ids[1] << 8 | tt.normal_ids[2] << 16 |
+                  static_cast<uint32_t>(tt.normal_ids[3]) << 24;
+    for (int k = 0; k < 4; ++k) out[48 + 4 * r + k] = tt.verts[k];
+}
+
+template <class T>
+int dalloc(T** p, uint64_t count, uint64_t& bytes) {
+    const size_t b = static_cast<size_t>(count ? count : 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), b);
+    if (e != cudaSuccess) return set_error(TV_ERR_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    bytes += b;
+    return TV_OK;
+}
+
+inline unsigned blocks(uint64_t n, unsigned t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+int finalize_grid(DeviceGrid& g, cudaStream_t st) {
+    const uint64_t nt = g.n_tets;
+    int rc;
+    uint64_t scratch_bytes = 0;
+    uint64_t *keys = nullptr, *keys_sorted = nullptr;
+    uint32_t *ids = nullptr, *order = nullptr, *is_int = nullptr, *tet2node = nullptr, *tet2leaf = nullptr,
+             *rootbuf = nullptr, *d_roots = nullptr;
+    int* d_depth = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0, t1 = 0, t2 = 0;
+    std::vector<uint32_t> hroot(24 + 24 + 96);
+
+    auto cleanup = [&]() {
+        cudaFree(keys), cudaFree(keys_sorted), cudaFree(ids), cudaFree(order), cudaFree(is_int);
+        cudaFree(tet2node), cudaFree(tet2leaf), cudaFree(rootbuf), cudaFree(d_roots), cudaFree(d_depth);
+        cudaFree(temp);
+    };
+#define TRY(x)            \
+    do {                  \
+        if ((rc = (x))) { \
+            cleanup();    \
+            return rc;    \
+        }                 \
+    } while (0)
+#define CK(x, what) TRY(cuda_status((x), what))
+
+    TRY(dalloc(&keys, nt, scratch_bytes));
+    TRY(dalloc(&keys_sorted, nt, scratch_bytes));
+    TRY(dalloc(&ids, nt, scratch_bytes));
+    TRY(dalloc(&order, nt, scratch_bytes));
+    TRY(dalloc(&is_int, nt, scratch_bytes));
+    TRY(dalloc(&tet2node, nt, scratch_bytes));
+    TRY(dalloc(&tet2leaf, nt, scratch_bytes));
+    TRY(dalloc(&rootbuf, 24 + 24 + 96, scratch_bytes));
+    TRY(dalloc(&d_roots, 24, scratch_bytes));
+    TRY(dalloc(&d_depth, 1, scratch_bytes));
+
+    keys_kernel<<<blocks(nt, 256), 256, 0, st>>>(g.tets, g.verts, nt, keys, ids, is_int);
+    CK(cudaGetLastError(), "keys_kernel");
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_sorted, ids, order, static_cast<int>(nt), 0, 64, st),
+       "sort sizing");
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, t2, is_int, tet2node, static_cast<int>(nt), st), "scan sizing");
+    temp_bytes = t1 > t2 ? t1 : t2;
+    CK(cudaMalloc(&temp, temp_bytes), "cudaMalloc temp");
+    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys, keys_sorted, ids, order, static_cast<int>(nt), 0, 64,
+                                       st),
+       "radix sort");
+    CK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, is_int, tet2node, static_cast<int>(nt), st), "scan");
+    CK(cudaMemsetAsync(tet2leaf, 0xff, nt * sizeof(uint32_t), st), "memset");
+    tet2leaf_kernel<<<blocks(g.n_leaves, 256), 256, 0, st>>>(order, g.n_leaves, tet2leaf);
+    CK(cudaGetLastError(), "tet2leaf_kernel");
+
+    TRY(dalloc(&g.leaves, g.n_leaves, g.bytes));
+    TRY(dalloc(&g.nodes, g.n_internal, g.bytes));
+    TRY(dalloc(&g.leaf2tet, g.n_leaves, g.bytes));
+    CK(cudaMemcpyAsync(g.leaf2tet, order, g.n_leaves * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "leaf2tet");
+    CK(cudaMemsetAsync(d_depth, 0, sizeof(int), st), "memset");
+    leaves_kernel<<<blocks(g.n_leaves, 256), 256, 0, st>>>(g.tets, order, tet2leaf, g.n_leaves, g.leaves, d_depth);
+    CK(cudaGetLastError(), "leaves_kernel");
+    nodes_kernel<<<blocks(nt, 256), 256, 0, st>>>(g.tets, g.verts, nt, tet2leaf, tet2node, g.nodes);
+    CK(cudaGetLastError(), "nodes_kernel");
+    CK(cudaMemcpyAsync(d_roots, g.roots, sizeof(g.roots), cudaMemcpyHostToDevice, st), "roots H2D");
+    roots_kernel<<<1, 32, 0, st>>>(g.tets, d_roots, tet2leaf, tet2node, rootbuf);
+    CK(cudaGetLastError(), "roots_kernel");
+    CK(cudaMemcpyAsync(hroot.data(), rootbuf, hroot.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st),
+       "roots D2H");
+    int depth = 0;
+    CK(cudaMemcpyAsync(&depth, d_depth, sizeof(int), cudaMemcpyDeviceToHost, st), "depth D2H");
+    CK(cudaStreamSynchronize(st), "finalize sync");
+    g.max_depth = depth;
+
+    GridView& v = g.view;
+    v.leaves = g.leaves;
+    v.nodes = g.nodes;
+    v.verts = g.verts;
+    v.leaf2tet = g.leaf2tet;
+    for (int r = 0; r < 24; ++r) {
+        v.root_ptr[r] = hroot[r];
+        v.root_nid[r] = hroot[24 + r];
+        for (int k = 0; k < 4; ++k) v.root_vid[r][k] = hroot[48 + 4 * r + k];
+    }
+    v.n_leaves = static_cast<uint32_t>(g.n_leaves);
+    v.n_nodes = static_cast<uint32_t>(g.n_internal);
+    cleanup();
+    return TV_OK;
+#undef CK
+#undef TRY
+}
+
+void free_grid(DeviceGrid& g) {
+    cudaFree(g.tets);
+    cudaFree(g.verts);
+    cudaFree(g.leaves);
+    cudaFree(g.nodes);
+    cudaFree(g.leaf2tet);
+    g.tets = nullptr;
+    g.verts = nullptr;
+    g.leaves = nullptr;
+    g.nodes = nullptr;
+    g.leaf2tet = nullptr;
+}
+
+}  // namespace tvb
