@@ -1,10 +1,40 @@
-// GPU LEB build (round-based, bit-exact with build_adaptive_grid) and the
-// on-device procedural fields.
+// GPU LEB build: build_adaptive_grid (builder.cpp:118-182) as synchronous
+// rounds, plus the on-device procedural fields.
+//
+// The reference refines from a (level, id) worklist with recursive conforming
+// propagation (tet_grid.cpp:384-426). Its final leaf set is a least fixed point
+// that does not depend on visiting order, so the GPU
+// computes it in rounds:
+//   eval     every fresh leaf gets its ownership statistics and criterion
+//            (builder.cpp:137-144); criterion leaves are marked;
+//   closure  bisect ALL marked leaves at once (tet_grid.cpp:339-382), then mark
+//            every leaf with a hanging edge (an edge whose integer midpoint
+//            already exists as a vertex); repeat until nothing is marked.
+// Rounds end when eval marks nothing. Tet and vertex ids are assigned by
+// order-preserving compaction and sorted dedup, so the build is deterministic;
+// they differ from the reference's allocation-order ids (F3), and parity is on
+// the canonical leaf set (sorted fixed-point corners + payload bits).
+//
+// Voxel ownership (builder.cpp:24-29) equals the pure locate_point partition
+// (SURVEY.md a18), so an owner map (one u32 per voxel) is maintained by the
+// same descent step locate_point uses (tet_grid.cpp:453-470). Per-leaf sums are
+// accumulated in parallel; because the reference sums in increasing voxel
+// index order, each decision / payload is certified against a rounding-error
+// bound and replayed sequentially in index order when the bound is ambiguous.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
 #include "tv_trace.cuh"
 
 namespace tvb {
 namespace {
 
+// ===================================================================== fields
 // cli.cpp:317-321
 __device__ double blob_density(double x, double y, double z) {
     const d3 d = sub(mk(x, y, z), mk(0.5, 0.5, 0.5));
@@ -58,7 +88,1200 @@ __global__ void gen_kernel(int kind, int nx, int ny, int nz, double value, float
     }
 }
 
+// ================================================================ LEB core
+typedef __int128 i128;
+
+__host__ __device__ inline int ep0(int e) { return e < 3 ? 0 : (e < 5 ? 1 : 2); }
+__host__ __device__ inline int ep1(int e) { return e < 3 ? e + 1 : (e < 5 ? e - 1 : 3); }
+
+// tet_grid.cpp:14-25
+__host__ __device__ inline i128 det_fixed(uint4 v0, uint4 v1, uint4 v2, uint4 v3) {
+    const int64_t a0 = static_cast<int64_t>(v1.x) - v0.x, a1 = static_cast<int64_t>(v1.y) - v0.y,
+                  a2 = static_cast<int64_t>(v1.z) - v0.z;
+    const int64_t b0 = static_cast<int64_t>(v2.x) - v0.x, b1 = static_cast<int64_t>(v2.y) - v0.y,
+                  b2 = static_cast<int64_t>(v2.z) - v0.z;
+    const int64_t c0 = static_cast<int64_t>(v3.x) - v0.x, c1 = static_cast<int64_t>(v3.y) - v0.y,
+                  c2 = static_cast<int64_t>(v3.z) - v0.z;
+    const int64_t m0 = b1 * c2 - b2 * c1, m1 = b2 * c0 - b0 * c2, m2 = b0 * c1 - b1 * c0;
+    return static_cast<i128>(a0) * m0 + static_cast<i128>(a1) * m1 + static_cast<i128>(a2) * m2;
+}
+
+// tet_grid.cpp:49-80; -1 = NotCanonical
+__host__ __device__ inline int face_normal_id(uint4 a, uint4 b, uint4 c, uint4 in) {
+    const int64_t u0 = static_cast<int64_t>(b.x) - a.x, u1 = static_cast<int64_t>(b.y) - a.y,
+                  u2 = static_cast<int64_t>(b.z) - a.z;
+    const int64_t v0 = static_cast<int64_t>(c.x) - a.x, v1 = static_cast<int64_t>(c.y) - a.y,
+                  v2 = static_cast<int64_t>(c.z) - a.z;
+    int64_t n[3] = {u1 * v2 - u2 * v1, u2 * v0 - u0 * v2, u0 * v1 - u1 * v0};
+    if (n[0] == 0 && n[1] == 0 && n[2] == 0) return -1;
+    const i128 side = static_cast<i128>(n[0]) * (static_cast<int64_t>(in.x) - a.x) +
+                      static_cast<i128>(n[1]) * (static_cast<int64_t>(in.y) - a.y) +
+                      static_cast<i128>(n[2]) * (static_cast<int64_t>(in.z) - a.z);
+    if (side == 0) return -1;
+    if (side > 0) n[0] = -n[0], n[1] = -n[1], n[2] = -n[2];
+    const int zeros = (n[0] == 0) + (n[1] == 0) + (n[2] == 0);
+    if (zeros == 2) {
+        for (int k = 0; k < 3; ++k)
+            if (n[k] != 0) return 2 * k + (n[k] > 0 ? 0 : 1);
+    } else if (zeros == 1) {
+        const int zk = n[0] == 0 ? 0 : (n[1] == 0 ? 1 : 2);
+        const int i = zk == 0 ? 1 : 0, j = zk == 2 ? 1 : 2;
+        const int64_t ai = n[i] < 0 ? -n[i] : n[i], aj = n[j] < 0 ? -n[j] : n[j];
+        if (ai != aj) return -1;
+        const int base = zk == 2 ? 6 : (zk == 1 ? 10 : 14);
+        const bool pi = n[i] > 0, pj = n[j] > 0;
+        if (pi && pj) return base;
+        if (!pi && !pj) return base + 1;
+        if (pi && !pj) return base + 2;
+        return base + 3;
+    }
+    return -1;
+}
+
+__host__ __device__ inline uint4 vq_of(const uint4* verts, uint32_t v) { return verts[v]; }
+
+// tet_grid.cpp:119-128
+__host__ __device__ inline bool compute_normals(tv_tet& t, const uint4* verts) {
+    for (int slot = 0; slot < 4; ++slot) {
+        uint4 f[3];
+        int n = 0;
+        for (int s = 0; s < 4; ++s)
+            if (s != slot) f[n++] = verts[t.verts[s]];
+        const int id = face_normal_id(f[0], f[1], f[2], verts[t.verts[slot]]);
+        if (id < 0) return false;
+        t.normal_ids[slot] = static_cast<uint8_t>(id);
+    }
+    return true;
+}
+
+// tet_grid.cpp:288-330
+__host__ __device__ inline void refinement_slots(const tv_tet& tt, const uint4* verts, int& s0, int& s1) {
+    int best = 0;
+    uint64_t best_len = 0;
+    uint32_t bmin = 0, bmax = 0;
+    for (int e = 0; e < 6; ++e) {
+        const uint32_t a = tt.verts[ep0(e)], b = tt.verts[ep1(e)];
+        const uint4 qa = verts[a], qb = verts[b];
+        const int64_t dx = static_cast<int64_t>(qa.x) - qb.x, dy = static_cast<int64_t>(qa.y) - qb.y,
+                      dz = static_cast<int64_t>(qa.z) - qb.z;
+        const uint64_t len = static_cast<uint64_t>(dx * dx) + static_cast<uint64_t>(dy * dy) +
+                             static_cast<uint64_t>(dz * dz);
+        const uint32_t mn = a < b ? a : b, mx = a < b ? b : a;
+        bool better;
+        if (e == 0) better = true;
+        else if (len != best_len) better = len > best_len;
+        else better = mn < bmin || (mn == bmin && mx < bmax);
+        if (better) best = e, best_len = len, bmin = mn, bmax = mx;
+    }
+    s0 = ep0(best);
+    s1 = ep1(best);
+}
+
+// ------------------------------------------------------------- vertex hash
+__device__ __forceinline__ uint64_t coord_hash(uint32_t x, uint32_t y, uint32_t z) {
+    return mix64((static_cast<uint64_t>(x) << 32 | y) ^ mix64(static_cast<uint64_t>(z) + 0x51ull));
+}
+
+__device__ uint32_t hash_find(const uint32_t* table, uint64_t mask, const uint4* verts, uint32_t x, uint32_t y,
+                              uint32_t z) {
+    uint64_t s = coord_hash(x, y, z) & mask;
+    for (;;) {
+        const uint32_t v = table[s];
+        if (v == kNone) return kNone;
+        const uint4 q = verts[v];
+        if (q.x == x && q.y == y && q.z == z) return v;
+        s = (s + 1) & mask;
+    }
+}
+
+// keys are distinct and absent: claim the first empty slot
+__device__ void hash_insert(uint32_t* table, uint64_t mask, uint32_t x, uint32_t y, uint32_t z, uint32_t vid) {
+    uint64_t s = coord_hash(x, y, z) & mask;
+    for (;;) {
+        if (atomicCAS(table + s, kNone, vid) == kNone) return;
+        s = (s + 1) & mask;
+    }
+}
+
+__global__ void hash_rebuild_kernel(uint32_t* table, uint64_t mask, const uint4* verts, uint32_t n) {
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const uint4 q = verts[v];
+    hash_insert(table, mask, q.x, q.y, q.z, v);
+}
+
+// ----------------------------------------------------------- build state
+enum : uint8_t { F_LEAF = 1, F_NEW = 2, F_EVAL = 4, F_MARK = 8 };
+enum : int { E_MIDPOINT = 1, E_NORMAL = 2, E_LEVEL = 4, E_FACE = 8 };
+
+struct Stats {
+    double sum, asum, tsum, tasum, lsum, lasum;
+    uint32_t cnt, mn, mx, pad;
+};
+static_assert(sizeof(Stats) == 64, "Stats is one 64-byte line");
+
+struct VolView {
+    const float* dens;
+    const float* temp;
+    const float* alb;
+    int nx, ny, nz;
+};
+
+struct CamCrit {
+    d3 pos;
+    double tan_half;
+    int h;
+    d3 pn[5];
+    double pd[5];
+};
+
+__device__ __forceinline__ uint32_t ord_f(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__device__ __forceinline__ d3 corner(const uint4* verts, uint32_t v) { return vpos(verts[v]); }
+
+// descent step at an internal tet (tet_grid.cpp:453-470) using its NodeRec
+__device__ __forceinline__ uint32_t descend_owner(const NodeRec* split, const tv_tet* tets, uint32_t cur, d3 p) {
+    while (tets[cur].children[0] != kNone) {
+        const NodeRec& nd = split[cur];
+        const double sp = dot(mk(nd.n[0], nd.n[1], nd.n[2]), sub(p, mk(nd.pm[0], nd.pm[1], nd.pm[2])));
+        const bool take_a = nd.sref_pos ? (sp >= 0.0) : (sp <= 0.0);
+        cur = take_a ? nd.child[0] : nd.child[1];
+    }
+    return cur;
+}
+
+struct RootScan {
+    uint32_t id[24];
+    uint32_t nid[24];
+    uint32_t vid[24][4];
+};
+
+// root scan (tet_grid.cpp:435-451) for every voxel centre
+__global__ void owner_init_kernel(RootScan R, const uint4* verts, int nx, int ny, int nz, uint32_t* owner) {
+    const uint64_t n = static_cast<uint64_t>(nx) * ny * nz;
+    for (uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; idx < n;
+         idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(idx % nx), j = static_cast<int>((idx / nx) % ny),
+                  k = static_cast<int>(idx / (static_cast<uint64_t>(nx) * ny));
+        const d3 p = mk((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz);
+        uint32_t cur = kNone;
+        double best = __longlong_as_double(0x7ff0000000000000ll);
+        for (int r = 0; r < 24; ++r) {
+            double worst = 0.0;
+            for (int slot = 0; slot < 4; ++slot) {
+                const uint32_t id = (R.nid[r] >> (8 * slot)) & 0xffu;
+                const d3 w = sub(p, vpos(verts[R.vid[r][(slot + 1) & 3]]));
+                worst = dmax(worst, ndot(id, w.x, w.y, w.z));
+            }
+            if (worst <= 1e-12) {
+                cur = R.id[r];
+                break;
+            }
+            if (worst < best) best = worst, cur = R.id[r];
+        }
+        owner[idx] = cur;
+    }
+}
+
+__global__ void owner_descend_kernel(const NodeRec* split, const tv_tet* tets, int nx, int ny, int nz,
+                                     uint32_t* owner) {
+    const uint64_t n = static_cast<uint64_t>(nx) * ny * nz;
+    for (uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; idx < n;
+         idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t o = owner[idx];
+        if (tets[o].children[0] == kNone) continue;
+        const int i = static_cast<int>(idx % nx), j = static_cast<int>((idx / nx) % ny),
+                  k = static_cast<int>(idx / (static_cast<uint64_t>(nx) * ny));
+        owner[idx] = descend_owner(split, tets, o, mk((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz));
+    }
+}
+
+__global__ void stats_zero_kernel(const uint32_t* list, uint32_t n, Stats* st, uint8_t* flags) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = list[i];
+    Stats z;
+    z.sum = z.asum = z.tsum = z.tasum = z.lsum = z.lasum = 0.0;
+    z.cnt = 0;
+    z.mn = 0xffffffffu;
+    z.mx = 0u;
+    z.pad = 0;
+    st[t] = z;
+    flags[t] |= F_EVAL;
+}
+
+constexpr int kRun = 16;  // voxels per thread along x
+
+__device__ __forceinline__ void flush(Stats* st, uint32_t L, const Stats& a, bool with_tl) {
+    Stats& s = st[L];
+    atomicAdd(&s.sum, a.sum);
+    atomicAdd(&s.asum, a.asum);
+    atomicAdd(&s.cnt, a.cnt);
+    atomicMin(&s.mn, a.mn);
+    atomicMax(&s.mx, a.mx);
+    if (with_tl) {
+        atomicAdd(&s.tsum, a.tsum);
+        atomicAdd(&s.tasum, a.tasum);
+        atomicAdd(&s.lsum, a.lsum);
+        atomicAdd(&s.lasum, a.lasum);
+    }
+}
+
+// Per-voxel accumulation of (count, min, max, sum, |sum|) into the owner leaf,
+// for leaves flagged F_EVAL. Each thread walks a run of kRun voxels along x and
+// flushes with atomics only when the owner changes.
+__global__ void stats_accum_kernel(VolView V, const uint32_t* owner, const uint8_t* flags, Stats* st, int with_tl) {
+    const uint64_t runs_x = (V.nx + kRun - 1) / kRun;
+    const uint64_t n = runs_x * V.ny * V.nz;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t row = r / runs_x;
+        const int i0 = static_cast<int>((r % runs_x) * kRun);
+        const uint64_t base = row * V.nx;
+        uint32_t cur = kNone;
+        Stats a{};
+        for (int i = i0; i < min(i0 + kRun, V.nx); ++i) {
+            const uint64_t idx = base + i;
+            const uint32_t L = owner[idx];
+            if (L != cur) {
+                if (cur != kNone && (flags[cur] & F_EVAL)) flush(st, cur, a, with_tl);
+                cur = L;
+                a.sum = a.asum = a.tsum = a.tasum = a.lsum = a.lasum = 0.0;
+                a.cnt = 0;
+                a.mn = 0xffffffffu;
+                a.mx = 0;
+            }
+            const float x = V.dens[idx];
+            a.sum += static_cast<double>(x);
+            a.asum += fabs(static_cast<double>(x));
+            a.cnt += 1;
+            a.mn = min(a.mn, ord_f(x));
+            a.mx = max(a.mx, ord_f(x));
+            if (with_tl) {
+                if (V.temp) {
+                    const double t = V.temp[idx];
+                    a.tsum += t;
+                    a.tasum += fabs(t);
+                }
+                if (V.alb) {
+                    const double l = V.alb[idx];
+                    a.lsum += l;
+                    a.lasum += fabs(l);
+                }
+            }
+        }
+        if (cur != kNone && (flags[cur] & F_EVAL)) flush(st, cur, a, with_tl);
+    }
+}
+
+// volume.cpp:47-66
+__device__ double trilinear(const float* data, int nx, int ny, int nz, d3 p) {
+    const double fx = p.x * nx - 0.5, fy = p.y * ny - 0.5, fz = p.z * nz - 0.5;
+    int i0 = static_cast<int>(floor(fx)), j0 = static_cast<int>(floor(fy)), k0 = static_cast<int>(floor(fz));
+    const double tx = fx - i0, ty = fy - j0, tz = fz - k0;
+    auto cl = [](int v, int n) { return v < 0 ? 0 : (v > n - 1 ? n - 1 : v); };
+    const int i1 = cl(i0 + 1, nx), j1 = cl(j0 + 1, ny), k1 = cl(k0 + 1, nz);
+    i0 = cl(i0, nx), j0 = cl(j0, ny), k0 = cl(k0, nz);
+    auto v = [&](int i, int j, int k) {
+        return static_cast<double>(data[(static_cast<uint64_t>(k) * ny + j) * nx + i]);
+    };
+    const double c00 = v(i0, j0, k0) * (1 - tx) + v(i1, j0, k0) * tx;
+    const double c10 = v(i0, j1, k0) * (1 - tx) + v(i1, j1, k0) * tx;
+    const double c01 = v(i0, j0, k1) * (1 - tx) + v(i1, j0, k1) * tx;
+    const double c11 = v(i0, j1, k1) * (1 - tx) + v(i1, j1, k1) * tx;
+    const double c0 = c00 * (1 - ty) + c10 * ty, c1 = c01 * (1 - ty) + c11 * ty;
+    return c0 * (1 - tz) + c1 * tz;
+}
+
+// Exact replay of aggregate_leaf's voxel loop (builder.cpp:37-79): AABB
+// centre range (volume.cpp:150-159), increasing index order k, j, i, sequential
+// double sums; ownership from the owner map.
+struct Exact {
+    double sum, tsum, lsum, mn, mx;
+    uint64_t cnt;
+};
+__device__ Exact exact_scan(const VolView& V, const uint32_t* owner, const tv_tet& tt, const uint4* verts,
+                            uint32_t leaf) {
+    d3 c[4];
+    for (int i = 0; i < 4; ++i) c[i] = corner(verts, tt.verts[i]);
+    d3 lo = c[0], hi = c[0];
+    for (int i = 1; i < 4; ++i) {
+        lo = mk(dmin(lo.x, c[i].x), dmin(lo.y, c[i].y), dmin(lo.z, c[i].z));
+        hi = mk(dmax(hi.x, c[i].x), dmax(hi.y, c[i].y), dmax(hi.z, c[i].z));
+    }
+    const int dims[3] = {V.nx, V.ny, V.nz};
+    const double l3[3] = {lo.x, lo.y, lo.z}, h3[3] = {hi.x, hi.y, hi.z};
+    int rlo[3], rhi[3];
+    for (int a = 0; a < 3; ++a) {
+        rlo[a] = max(0, static_cast<int>(ceil(l3[a] * dims[a] - 0.5 - 1e-12)));
+        rhi[a] = min(dims[a] - 1, static_cast<int>(floor(h3[a] * dims[a] - 0.5 + 1e-12)));
+    }
+    Exact e{0.0, 0.0, 0.0, __longlong_as_double(0x7ff0000000000000ll), -__longlong_as_double(0x7ff0000000000000ll),
+            0};
+    for (int k = rlo[2]; k <= rhi[2]; ++k)
+        for (int j = rlo[1]; j <= rhi[1]; ++j)
+            for (int i = rlo[0]; i <= rhi[0]; ++i) {
+                const uint64_t idx = (static_cast<uint64_t>(k) * V.ny + j) * V.nx + i;
+                if (owner[idx] != leaf) continue;
+                const double v = V.dens[idx];
+                e.mn = dmin(e.mn, v);
+                e.mx = dmax(e.mx, v);
+                e.sum += v;
+                if (V.temp) e.tsum += V.temp[idx];
+                if (V.alb) e.lsum += V.alb[idx];
+                ++e.cnt;
+            }
+    return e;
+}
+
+__device__ __forceinline__ double err_bound(double n, double asum) {
+    // |sequential - any-order sum| <= 2 (n-1) u sum|x| (+ second order); padded
+    return (2.0 * n + 4.0) * 0x1.0p-53 * asum * (1.0 + 0x1.0p-30);
+}
+
+__device__ __forceinline__ bool crit_var(double mx, double mn, double sum, double n, double thr) {
+    const double mean = sum / n;
+    const double var = mean == 0.0 ? 0.0 : (mx - mn) / mean;  // volume.cpp:196-199
+    return var > thr;
+}
+
+// camera.cpp:57-68, 70-85
+__device__ bool outside_frustum(const CamCrit& C, const d3* cs) {
+    for (int p = 0; p < 5; ++p) {
+        bool all_out = true;
+        for (int i = 0; i < 4; ++i)
+            if (dot(C.pn[p], cs[i]) >= C.pd[p]) {
+                all_out = false;
+                break;
+            }
+        if (all_out) return true;
+    }
+    return false;
+}
+__device__ double projected_size(const CamCrit& C, const d3* cs) {
+    double longest_sq = 0.0;
+    for (int e = 0; e < 6; ++e) {
+        const d3 d = sub(cs[ep0(e)], cs[ep1(e)]);
+        longest_sq = dmax(longest_sq, dot(d, d));
+    }
+    const double longest = sqrt(longest_sq);
+    const d3 cen = mul(add(add(add(cs[0], cs[1]), cs[2]), cs[3]), 0.25);
+    double rsq = 0.0;
+    for (int i = 0; i < 4; ++i) {
+        const d3 d = sub(cs[i], cen);
+        rsq = dmax(rsq, dot(d, d));
+    }
+    const d3 tc = sub(cen, C.pos);
+    if (dot(tc, tc) <= rsq) return __longlong_as_double(0x7ff0000000000000ll);
+    const double dist = dmax(sqrt(dot(tc, tc)), 1e-4);
+    return longest / (2.0 * dist * C.tan_half) * C.h;
+}
+
+struct EvalParams {
+    double thr;
+    int max_level;
+    int use_camera;
+    double pixel_thr;
+    CamCrit cam;
+};
+
+// builder.cpp:134-144 for every fresh leaf
+__global__ void eval_kernel(const uint32_t* list, uint32_t n, VolView V, const uint32_t* owner, const tv_tet* tets,
+                            const uint4* verts, const Stats* st, EvalParams E, uint8_t* flags,
+                            unsigned long long* counters /* [0] replays [1] voxel visits */) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = list[i];
+    const tv_tet tt = tets[t];
+    const Stats s = st[t];
+    flags[t] &= static_cast<uint8_t>(~F_EVAL);
+    atomicAdd(counters + 1, static_cast<unsigned long long>(s.cnt));
+    if (s.cnt == 0) return;  // trilinear fallback: min == max == mean -> variation 0
+    const double nn = static_cast<double>(s.cnt);
+    const double mn = unord_f(s.mn), mx = unord_f(s.mx);
+    bool split;
+    const double B = err_bound(nn, s.asum);
+    const double lo = __dsub_rd(s.sum, B), hi = __dadd_ru(s.sum, B);
+    if (B == 0.0) {
+        split = crit_var(mx, mn, s.sum, nn, E.thr);
+    } else if (((lo > 0.0 && hi > 0.0) || (lo < 0.0 && hi < 0.0)) &&
+               crit_var(mx, mn, lo, nn, E.thr) == crit_var(mx, mn, hi, nn, E.thr)) {
+        split = crit_var(mx, mn, lo, nn, E.thr);
+    } else {  // ambiguous under the bound: replay the reference's sequential sum
+        atomicAdd(counters, 1ull);
+        const Exact e = exact_scan(V, owner, tt, verts, t);
+        split = crit_var(e.mx, e.mn, e.sum, static_cast<double>(e.cnt), E.thr);
+    }
+    if (!split) return;
+    if (tt.level >= E.max_level) return;
+    if (E.use_camera) {
+        d3 cs[4];
+        for (int k = 0; k < 4; ++k) cs[k] = corner(verts, tt.verts[k]);
+        if (outside_frustum(E.cam, cs)) return;
+        if (!(projected_size(E.cam, cs) > E.pixel_thr)) return;
+    }
+    flags[t] |= F_MARK;
+}
+
+// midpoint of each marked leaf's refinement edge: existing vertex id, or a
+// "missing" record for sorted dedup
+__global__ void midpoint_kernel(const uint32_t* marked, uint32_t n, const tv_tet* tets, const uint4* verts,
+                                const uint32_t* table, uint64_t mask, uint32_t* mid_vid, uint64_t* miss_hi,
+                                uint32_t* miss_lo, uint32_t* miss_idx, uint32_t* n_miss, int* err) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const tv_tet tt = tets[marked[i]];
+    int s0, s1;
+    refinement_slots(tt, verts, s0, s1);
+    const uint4 a = verts[tt.verts[s0]], b = verts[tt.verts[s1]];
+    const uint64_t sx = static_cast<uint64_t>(a.x) + b.x, sy = static_cast<uint64_t>(a.y) + b.y,
+                   sz = static_cast<uint64_t>(a.z) + b.z;
+    if ((sx | sy | sz) & 1u) {  // tet_grid.cpp:353
+        atomicOr(err, E_MIDPOINT);
+        mid_vid[i] = kNone;
+        return;
+    }
+    const uint32_t mx = static_cast<uint32_t>(sx / 2), my = static_cast<uint32_t>(sy / 2),
+                   mz = static_cast<uint32_t>(sz / 2);
+    const uint32_t v = hash_find(table, mask, verts, mx, my, mz);
+    mid_vid[i] = v;
+    if (v == kNone) {
+        const uint32_t k = atomicAdd(n_miss, 1u);
+        miss_hi[k] = static_cast<uint64_t>(mx) << 25 | my;
+        miss_lo[k] = mz;
+        miss_idx[k] = i;
+    }
+}
+
+__global__ void dedup_heads_kernel(const uint64_t* hi, const uint32_t* lo, uint32_t n, uint32_t* head) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    head[i] = (i == 0 || hi[i] != hi[i - 1] || lo[i] != lo[i - 1]) ? 1u : 0u;
+}
+
+// scan[i] = inclusive count of heads -> vertex id n_v + scan[i] - 1
+__global__ void dedup_assign_kernel(const uint64_t* hi, const uint32_t* lo, const uint32_t* idx, const uint32_t* head,
+                                    const uint32_t* scan, uint32_t n, uint32_t n_v, uint4* verts, uint32_t* table,
+                                    uint64_t mask, uint32_t* mid_vid) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t vid = n_v + scan[i] - 1;
+    mid_vid[idx[i]] = vid;
+    if (head[i]) {
+        const uint32_t x = static_cast<uint32_t>(hi[i] >> 25), y = static_cast<uint32_t>(hi[i] & 0x1ffffffull),
+                       z = lo[i];
+        verts[vid] = make_uint4(x, y, z, 0);
+        hash_insert(table, mask, x, y, z, vid);
+    }
+}
+
+// tet_grid.cpp:339-382 for all marked leaves at once; children get ids
+// n_t + 2i, n_t + 2i + 1 in marked-list (ascending id) order.
+__global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, tv_tet* tets, const uint4* verts,
+                              const uint32_t* mid_vid, NodeRec* split, uint8_t* flags, uint8_t* vtouch, int max_level,
+                              int* err) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = marked[i];
+    const tv_tet parent = tets[t];
+    if (parent.level >= max_level) atomicOr(err, E_LEVEL);  // MaxLevelExceeded (tet_grid.cpp:342)
+    int s0, s1;
+    refinement_slots(parent, verts, s0, s1);
+    const uint32_t vm = mid_vid[i];
+    const uint32_t ida = n_t + 2 * i, idb = ida + 1;
+    tv_tet a = parent, b = parent;
+    a.verts[s1] = vm;
+    b.verts[s0] = vm;
+    tv_tet* cs[2] = {&a, &b};
+    for (int k = 0; k < 2; ++k) {
+        tv_tet* c = cs[k];
+        c->parent = t;
+        c->children[0] = c->children[1] = kNone;
+        c->neighbors[0] = c->neighbors[1] = c->neighbors[2] = c->neighbors[3] = kNone;
+        c->level = static_cast<uint8_t>(parent.level + 1);
+        c->density = c->temperature = c->albedo = 0.0f;
+        c->mask = 0;
+        if (!compute_normals(*c, verts)) atomicOr(err, E_NORMAL);
+    }
+    tets[ida] = a;
+    tets[idb] = b;
+    tets[t].children[0] = ida;
+    tets[t].children[1] = idb;
+    tets[t].neighbors[0] = tets[t].neighbors[1] = tets[t].neighbors[2] = tets[t].neighbors[3] = kNone;
+    flags[ida] = F_LEAF | F_NEW;
+    flags[idb] = F_LEAF | F_NEW;
+    flags[t] = 0;
+    vtouch[parent.verts[s0]] = 1;
+    vtouch[parent.verts[s1]] = 1;
+    // split plane for the owner-map descent (tet_grid.cpp:453-470)
+    const d3 pm = vpos(verts[vm]);
+    int oa = -1, ob = -1;
+    for (int s = 0; s < 4; ++s)
+        if (s != s0 && s != s1) {
+            if (oa < 0) oa = s;
+            else ob = s;
+        }
+    const d3 pa = vpos(verts[parent.verts[oa]]), pb = vpos(verts[parent.verts[ob]]);
+    const d3 nn = cross(sub(pa, pm), sub(pb, pm));
+    const double sref = dot(nn, sub(vpos(verts[parent.verts[s0]]), pm));
+    NodeRec r;
+    r.n[0] = nn.x, r.n[1] = nn.y, r.n[2] = nn.z;
+    r.pm[0] = pm.x, r.pm[1] = pm.y, r.pm[2] = pm.z;
+    r.child[0] = ida;
+    r.child[1] = idb;
+    r.sref_pos = sref > 0.0 ? 1u : 0u;
+    r.pad = 0;
+    split[t] = r;
+}
+
+// mark leaves with a hanging edge; only leaves that are new or have >= 2
+// vertices touched by the last bisect pass can have one
+__global__ void hanging_kernel(const uint32_t* leaves, uint32_t n, const tv_tet* tets, const uint4* verts,
+                               const uint32_t* table, uint64_t mask, const uint8_t* vtouch, uint8_t* flags,
+                               uint32_t* n_marked) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = leaves[i];
+    const tv_tet tt = tets[t];
+    const uint8_t f = flags[t];
+    if (!(f & F_NEW)) {
+        const int touched = vtouch[tt.verts[0]] + vtouch[tt.verts[1]] + vtouch[tt.verts[2]] + vtouch[tt.verts[3]];
+        if (touched < 2) return;
+    }
+    uint4 q[4];
+    for (int k = 0; k < 4; ++k) q[k] = verts[tt.verts[k]];
+    for (int e = 0; e < 6; ++e) {
+        const uint4 a = q[ep0(e)], b = q[ep1(e)];
+        const uint64_t sx = static_cast<uint64_t>(a.x) + b.x, sy = static_cast<uint64_t>(a.y) + b.y,
+                       sz = static_cast<uint64_t>(a.z) + b.z;
+        if ((sx | sy | sz) & 1u) continue;
+        if (hash_find(table, mask, verts, static_cast<uint32_t>(sx / 2), static_cast<uint32_t>(sy / 2),
+                      static_cast<uint32_t>(sz / 2)) != kNone) {
+            flags[t] = f | F_MARK;
+            atomicAdd(n_marked, 1u);
+            return;
+        }
+    }
+}
+
+__global__ void flag_select_kernel(const uint8_t* flags, uint32_t n, uint8_t bit, uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (flags[i] & bit) ? 1 : 0;
+}
+__global__ void list_flag_kernel(const uint32_t* list, uint32_t n, const uint8_t* flags, uint8_t bit, uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (flags[list[i]] & bit) ? 1 : 0;
+}
+__global__ void clear_flag_kernel(const uint32_t* list, uint32_t n, uint8_t* flags, uint8_t bit) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flags[list[i]] &= static_cast<uint8_t>(~bit);
+}
+__global__ void iota_kernel(uint32_t* out, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+struct PayloadParams {
+    double scale;
+    int has_t, has_a;
+};
+
+// assign_payloads (builder.cpp:164-182): certified against the parallel sums,
+// replayed sequentially when the float rounding is ambiguous.
+__global__ void payload_kernel(const uint32_t* list, uint32_t n, VolView V, const uint32_t* owner, tv_tet* tets,
+                               const uint4* verts, const Stats* st, PayloadParams P, unsigned long long* replays,
+                               int* max_depth) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = list[i];
+    tv_tet tt = tets[t];
+    const Stats s = st[t];
+    atomicMax(max_depth, static_cast<int>(tt.level));
+    float dens, temp = 0.f, alb = 0.f;
+    if (s.cnt == 0) {
+        d3 c[4];
+        for (int k = 0; k < 4; ++k) c[k] = corner(verts, tt.verts[k]);
+        const d3 cen = mul(add(add(add(c[0], c[1]), c[2]), c[3]), 0.25);
+        const double m = trilinear(V.dens, V.nx, V.ny, V.nz, cen);
+        dens = static_cast<float>(P.scale * m);
+        if (P.has_t) temp = static_cast<float>(trilinear(V.temp, V.nx, V.ny, V.nz, cen));
+        if (P.has_a) alb = static_cast<float>(dclamp(trilinear(V.alb, V.nx, V.ny, V.nz, cen), 0.0, 1.0));
+    } else {
+        const double nn = static_cast<double>(s.cnt);
+        bool ok = true;
+        auto fdens = [&](double x) { return static_cast<float>(P.scale * (x / nn)); };
+        auto ftemp = [&](double x) { return static_cast<float>(x / nn); };
+        auto falb = [&](double x) { return static_cast<float>(dclamp(x / nn, 0.0, 1.0)); };
+        const double B = err_bound(nn, s.asum);
+        dens = fdens(s.sum);
+        if (B > 0.0 && fdens(__dsub_rd(s.sum, B)) != fdens(__dadd_ru(s.sum, B))) ok = false;
+        if (P.has_t) {
+            const double Bt = err_bound(nn, s.tasum);
+            temp = ftemp(s.tsum);
+            if (Bt > 0.0 && ftemp(__dsub_rd(s.tsum, Bt)) != ftemp(__dadd_ru(s.tsum, Bt))) ok = false;
+        }
+        if (P.has_a) {
+            const double Ba = err_bound(nn, s.lasum);
+            alb = falb(s.lsum);
+            if (Ba > 0.0 && falb(__dsub_rd(s.lsum, Ba)) != falb(__dadd_ru(s.lsum, Ba))) ok = false;
+        }
+        if (!ok) {
+            atomicAdd(replays, 1ull);
+            const Exact e = exact_scan(V, owner, tt, verts, t);
+            const double en = static_cast<double>(e.cnt);
+            dens = static_cast<float>(P.scale * (e.sum / en));
+            if (P.has_t) temp = static_cast<float>(e.tsum / en);
+            if (P.has_a) alb = static_cast<float>(dclamp(e.lsum / en, 0.0, 1.0));
+        }
+    }
+    tt.density = dens;
+    tt.mask = 1;
+    if (P.has_t) tt.temperature = temp, tt.mask |= 2;
+    if (P.has_a) tt.albedo = alb, tt.mask |= 4;
+    tets[t].density = tt.density;
+    tets[t].temperature = tt.temperature;
+    tets[t].albedo = tt.albedo;
+    tets[t].mask = tt.mask;
+}
+
+// face records for neighbour pairing: key = sorted vertex triple
+__global__ void face_keys_kernel(const uint32_t* leaves, uint32_t n, const tv_tet* tets, uint64_t* khi, uint32_t* klo,
+                                 uint32_t* rec) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t t = leaves[i];
+    const tv_tet tt = tets[t];
+    for (int slot = 0; slot < 4; ++slot) {
+        uint32_t k[3];
+        int m = 0;
+        for (int s = 0; s < 4; ++s)
+            if (s != slot) k[m++] = tt.verts[s];
+        if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
+        if (k[1] > k[2]) { uint32_t x = k[1]; k[1] = k[2]; k[2] = x; }
+        if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
+        const uint64_t o = 4ull * i + slot;
+        khi[o] = static_cast<uint64_t>(k[0]) << 32 | k[1];
+        klo[o] = k[2];
+        rec[o] = static_cast<uint32_t>(o);
+    }
+}
+
+__global__ void face_pair_kernel(const uint64_t* khi, const uint32_t* klo, const uint32_t* rec, uint64_t n,
+                                 const uint32_t* leaves, tv_tet* tets, int* err) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const bool eq_prev = i > 0 && khi[i] == khi[i - 1] && klo[i] == klo[i - 1];
+    const bool eq_next = i + 1 < n && khi[i] == khi[i + 1] && klo[i] == klo[i + 1];
+    const uint32_t r = rec[i];
+    const uint32_t t = leaves[r >> 2], slot = r & 3;
+    if (eq_prev && eq_next) {
+        atomicOr(err, E_FACE);  // face shared by more than two leaves
+        return;
+    }
+    uint32_t other = kNone;
+    if (eq_prev) other = leaves[rec[i - 1] >> 2];
+    if (eq_next) other = leaves[rec[i + 1] >> 2];
+    tets[t].neighbors[slot] = other;
+}
+
+// keys of the refinement-edge midpoint for marked[idx[p]] in position p
+__global__ void regather_kernel(const uint32_t* idx, const uint32_t* marked, uint32_t n, const tv_tet* tets,
+                                const uint4* verts, uint64_t* hi, uint32_t* lo) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const tv_tet tt = tets[marked[idx[p]]];
+    int s0, s1;
+    refinement_slots(tt, verts, s0, s1);
+    const uint4 a = verts[tt.verts[s0]], b = verts[tt.verts[s1]];
+    const uint32_t mx = static_cast<uint32_t>((static_cast<uint64_t>(a.x) + b.x) / 2),
+                   my = static_cast<uint32_t>((static_cast<uint64_t>(a.y) + b.y) / 2),
+                   mz = static_cast<uint32_t>((static_cast<uint64_t>(a.z) + b.z) / 2);
+    hi[p] = static_cast<uint64_t>(mx) << 25 | my;
+    lo[p] = mz;
+}
+
+// face key of face record rec[p] (4 * leaf-list index + slot)
+__global__ void gather_face_hi_kernel(const uint32_t* rec, uint64_t n, const uint32_t* leaves, const tv_tet* tets,
+                                      uint64_t* khi, uint32_t* klo) {
+    const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (p >= n) return;
+    const uint32_t r = rec[p];
+    const tv_tet& tt = tets[leaves[r >> 2]];
+    const int slot = r & 3;
+    uint32_t k[3];
+    int m = 0;
+    for (int s = 0; s < 4; ++s)
+        if (s != slot) k[m++] = tt.verts[s];
+    if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
+    if (k[1] > k[2]) { uint32_t x = k[1]; k[1] = k[2]; k[2] = x; }
+    if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
+    khi[p] = static_cast<uint64_t>(k[0]) << 32 | k[1];
+    klo[p] = k[2];
+}
+
+// ------------------------------------------------------------ host side
+inline unsigned nblk(uint64_t n, unsigned t = 256) { return static_cast<unsigned>(std::max<uint64_t>((n + t - 1) / t, 1)); }
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~Buf() { cudaFree(p); }
+    template <class T>
+    T* as() {
+        return static_cast<T*>(p);
+    }
+};
+
+int ensure(Buf& b, size_t bytes, bool keep = false) {
+    if (b.bytes >= bytes) return TV_OK;
+    size_t nb = std::max(bytes, b.bytes + b.bytes / 2);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, nb);
+    if (e != cudaSuccess) return cuda_status(e, "build alloc");
+    if (keep && b.p && b.bytes) {
+        e = cudaMemcpy(p, b.p, b.bytes, cudaMemcpyDeviceToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            return cuda_status(e, "build grow");
+        }
+    }
+    cudaFree(b.p);
+    b.p = p;
+    b.bytes = nb;
+    return TV_OK;
+}
+
+// host init_roots (tet_grid.cpp:184-233)
+int host_init_roots(std::vector<uint4>& verts, std::vector<tv_tet>& tets, uint32_t roots[24]) {
+    auto intern = [&](uint32_t x, uint32_t y, uint32_t z) {
+        for (uint32_t i = 0; i < verts.size(); ++i)
+            if (verts[i].x == x && verts[i].y == y && verts[i].z == z) return i;
+        verts.push_back(make_uint4(x, y, z, 0));
+        return static_cast<uint32_t>(verts.size() - 1);
+    };
+    const uint32_t S = 1u << 24, H = S / 2;
+    const uint32_t center = intern(H, H, H);
+    int ri = 0;
+    for (int axis = 0; axis < 3; ++axis)
+        for (int side = 0; side < 2; ++side) {
+            uint32_t fc[3] = {H, H, H};
+            fc[axis] = side ? S : 0;
+            const uint32_t fcv = intern(fc[0], fc[1], fc[2]);
+            const int u = axis == 0 ? 1 : 0, w = axis == 2 ? 1 : 2;
+            const uint32_t ring[4][2] = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+            uint32_t corner_v[4];
+            for (int k = 0; k < 4; ++k) {
+                uint32_t c[3] = {0, 0, 0};
+                c[axis] = side ? S : 0;
+                c[u] = ring[k][0] * S;
+                c[w] = ring[k][1] * S;
+                corner_v[k] = intern(c[0], c[1], c[2]);
+            }
+            for (int k = 0; k < 4; ++k) {
+                uint32_t p = corner_v[k], q = corner_v[(k + 1) % 4];
+                if (det_fixed(verts[p], verts[fcv], verts[center], verts[q]) < 0) std::swap(p, q);
+                tv_tet t;
+                std::memset(&t, 0, sizeof t);
+                t.verts[0] = p, t.verts[1] = fcv, t.verts[2] = center, t.verts[3] = q;
+                t.children[0] = t.children[1] = t.parent = TV_NO_TET;
+                for (int f = 0; f < 4; ++f) t.neighbors[f] = TV_NO_TET;
+                roots[ri++] = static_cast<uint32_t>(tets.size());
+                tets.push_back(t);
+            }
+        }
+    for (auto& t : tets)
+        if (!compute_normals(t, verts.data())) return set_error(TV_ERR_GRID, "root normals not canonical");
+    return TV_OK;
+}
+
+int validate_build_cfg(const tv_build_config* c) {  // builder.cpp:12-17
+    if (!c) return set_error(TV_ERR_ARG, "build config is null");
+    if (!(c->variation_threshold >= 0.0)) return set_error(TV_ERR_CONFIG, "variationThreshold must be >= 0");
+    if (c->max_level < 0 || c->max_level > 48) return set_error(TV_ERR_CONFIG, "maxLevel out of range");
+    if (!(c->pixel_threshold > 0.0)) return set_error(TV_ERR_CONFIG, "pixelThreshold must be > 0");
+    if (!(c->density_scale >= 0.0)) return set_error(TV_ERR_CONFIG, "densityScale must be >= 0");
+    return TV_OK;
+}
+
 }  // namespace
+
+// defined in tv_capi.cu
+int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]);
+
+int build_grid(const float* dens, const float* temp, const float* alb, int nx, int ny, int nz,
+               const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out, tv_build_stats* stats) {
+    int rc = validate_build_cfg(cfg);
+    if (rc) return rc;
+    if (cfg->use_camera && !camera) return set_error(TV_ERR_CONFIG, "useCamera set but no camera given");
+    if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR_CONFIG, "volume dimensions must be positive");
+    EvalParams E{};
+    E.thr = cfg->variation_threshold;
+    E.max_level = cfg->max_level;
+    E.use_camera = cfg->use_camera;
+    E.pixel_thr = cfg->pixel_threshold;
+    if (camera) {
+        CamView cv;
+        d3 pn[5];
+        double pd[5];
+        if ((rc = host_camera(camera, cv, pn, pd))) return rc;
+        E.cam.pos = mk(cv.pos[0], cv.pos[1], cv.pos[2]);
+        E.cam.tan_half = cv.tan_half;
+        E.cam.h = cv.h;
+        for (int i = 0; i < 5; ++i) E.cam.pn[i] = pn[i], E.cam.pd[i] = pd[i];
+    }
+    const int grid_max_level = std::max(cfg->max_level, 1);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+
+    const uint64_t nvox = static_cast<uint64_t>(nx) * ny * nz;
+    VolView V{dens, temp, alb, nx, ny, nz};
+    Buf tets_b, verts_b, split_b, flags_b, stats_b, table_b, vtouch_b, owner_b, list_b, list2_b, leaves_b, sel_b,
+        tmp_b, mid_b, miss_hi_b, miss_lo_b, miss_idx_b, miss_hi2_b, miss_lo2_b, miss_idx2_b, head_b, scan_b, misc_b;
+    size_t cap_t = 0, cap_v = 0;
+    uint64_t hmask = 0;
+
+    std::vector<uint4> hv;
+    std::vector<tv_tet> ht;
+    uint32_t roots[24];
+    if ((rc = host_init_roots(hv, ht, roots))) return rc;
+    uint32_t n_t = static_cast<uint32_t>(ht.size()), n_v = static_cast<uint32_t>(hv.size());
+
+#define TRY(x)                 \
+    do {                       \
+        if ((rc = (x))) return rc; \
+    } while (0)
+#define CK(x, what) TRY(cuda_status((x), what))
+
+    auto grow_tets = [&](size_t need) -> int {
+        if (need <= cap_t) return TV_OK;
+        const size_t nc = std::max(need, cap_t * 2 + 1024);
+        TRY(ensure(tets_b, nc * sizeof(tv_tet), true));
+        TRY(ensure(split_b, nc * sizeof(NodeRec), true));
+        TRY(ensure(flags_b, nc, true));
+        TRY(ensure(stats_b, nc * sizeof(Stats), true));
+        cap_t = nc;
+        return TV_OK;
+    };
+    auto grow_verts = [&](size_t need) -> int {
+        if (need <= cap_v) return TV_OK;
+        const size_t nc = std::max(need, cap_v * 2 + 1024);
+        TRY(ensure(verts_b, nc * sizeof(uint4), true));
+        TRY(ensure(vtouch_b, nc, true));
+        size_t slots = 1024;
+        while (slots < 2 * nc) slots <<= 1;
+        TRY(ensure(table_b, slots * sizeof(uint32_t)));
+        CK(cudaMemset(table_b.p, 0xff, slots * sizeof(uint32_t)), "hash clear");
+        hmask = slots - 1;
+        hash_rebuild_kernel<<<nblk(n_v), 256>>>(table_b.as<uint32_t>(), hmask, verts_b.as<uint4>(), n_v);
+        CK(cudaGetLastError(), "hash rebuild");
+        cap_v = nc;
+        return TV_OK;
+    };
+
+    // initial capacity guess: grows geometrically as needed
+    TRY(grow_tets(std::max<size_t>(1 << 16, nvox / 4)));
+    CK(cudaMemcpy(tets_b.p, ht.data(), ht.size() * sizeof(tv_tet), cudaMemcpyHostToDevice), "roots H2D");
+    {
+        const size_t need_v = std::max<size_t>(1 << 15, nvox / 16);
+        TRY(ensure(verts_b, need_v * sizeof(uint4)));
+        CK(cudaMemcpy(verts_b.p, hv.data(), hv.size() * sizeof(uint4), cudaMemcpyHostToDevice), "verts H2D");
+        TRY(grow_verts(need_v));
+    }
+    CK(cudaMemset(flags_b.p, 0, cap_t), "flags");
+    {
+        std::vector<uint8_t> f(n_t, F_LEAF | F_NEW);
+        CK(cudaMemcpy(flags_b.p, f.data(), n_t, cudaMemcpyHostToDevice), "flags H2D");
+    }
+    TRY(ensure(owner_b, nvox * sizeof(uint32_t)));
+    TRY(ensure(misc_b, 64));
+    int* d_err = misc_b.as<int>();
+    uint32_t* d_cnt = reinterpret_cast<uint32_t*>(misc_b.as<char>() + 8);
+    unsigned long long* d_ctr = reinterpret_cast<unsigned long long*>(misc_b.as<char>() + 16);  // replays, visits
+    int* d_depth = reinterpret_cast<int*>(misc_b.as<char>() + 32);
+    CK(cudaMemset(misc_b.p, 0, 64), "misc");
+
+    RootScan R;
+    for (int r = 0; r < 24; ++r) {
+        R.id[r] = roots[r];
+        const tv_tet& t = ht[roots[r]];
+        R.nid[r] = t.normal_ids[0] | t.normal_ids[1] << 8 | t.normal_ids[2] << 16 |
+                   static_cast<uint32_t>(t.normal_ids[3]) << 24;
+        for (int k = 0; k < 4; ++k) R.vid[r][k] = t.verts[k];
+    }
+    owner_init_kernel<<<148 * 8, 256>>>(R, verts_b.as<uint4>(), nx, ny, nz, owner_b.as<uint32_t>());
+    CK(cudaGetLastError(), "owner init");
+
+    // device lists
+    auto select_flagged = [&](const uint32_t* in_list, uint32_t n_in, uint8_t bit, Buf& outb, uint32_t& n_out,
+                              bool from_all) -> int {
+        TRY(ensure(sel_b, std::max<size_t>(n_in, 1)));
+        TRY(ensure(outb, std::max<size_t>(n_in, 1) * sizeof(uint32_t)));
+        if (from_all) {
+            flag_select_kernel<<<nblk(n_in), 256>>>(flags_b.as<uint8_t>(), n_in, bit, sel_b.as<uint8_t>());
+        } else {
+            list_flag_kernel<<<nblk(n_in), 256>>>(in_list, n_in, flags_b.as<uint8_t>(), bit, sel_b.as<uint8_t>());
+        }
+        CK(cudaGetLastError(), "flag kernel");
+        const uint32_t* src = in_list;
+        if (from_all) {
+            TRY(ensure(list2_b, std::max<size_t>(n_in, 1) * sizeof(uint32_t)));
+            iota_kernel<<<nblk(n_in), 256>>>(list2_b.as<uint32_t>(), n_in);
+            src = list2_b.as<uint32_t>();
+        }
+        size_t tb = 0;
+        CK(cub::DeviceSelect::Flagged(nullptr, tb, src, sel_b.as<uint8_t>(), outb.as<uint32_t>(), d_cnt,
+                                      static_cast<int>(n_in)),
+           "select sizing");
+        TRY(ensure(tmp_b, tb));
+        CK(cub::DeviceSelect::Flagged(tmp_b.p, tb, src, sel_b.as<uint8_t>(), outb.as<uint32_t>(), d_cnt,
+                                      static_cast<int>(n_in)),
+           "select");
+        CK(cudaMemcpy(&n_out, d_cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost), "select count");
+        return TV_OK;
+    };
+
+    uint64_t crit = 0, bisections = 0, passes = 0, replays = 0;
+    int rounds = 0;
+    uint32_t n_fresh = 24, n_marked = 0, n_leaves = 24;
+    Buf fresh_b, marked_b;
+    TRY(ensure(fresh_b, 24 * sizeof(uint32_t)));
+    CK(cudaMemcpy(fresh_b.p, roots, sizeof(roots), cudaMemcpyHostToDevice), "fresh");
+    int herr = 0;
+
+    for (;;) {
+        // ---- eval fresh leaves ----
+        if (rounds > 0) {
+            owner_descend_kernel<<<148 * 8, 256>>>(split_b.as<NodeRec>(), tets_b.as<tv_tet>(), nx, ny, nz,
+                                                   owner_b.as<uint32_t>());
+            CK(cudaGetLastError(), "owner descend");
+        }
+        clear_flag_kernel<<<nblk(n_fresh), 256>>>(fresh_b.as<uint32_t>(), n_fresh, flags_b.as<uint8_t>(), F_NEW);
+        stats_zero_kernel<<<nblk(n_fresh), 256>>>(fresh_b.as<uint32_t>(), n_fresh, stats_b.as<Stats>(),
+                                                  flags_b.as<uint8_t>());
+        stats_accum_kernel<<<148 * 8, 256>>>(V, owner_b.as<uint32_t>(), flags_b.as<uint8_t>(), stats_b.as<Stats>(), 0);
+        eval_kernel<<<nblk(n_fresh, 128), 128>>>(fresh_b.as<uint32_t>(), n_fresh, V, owner_b.as<uint32_t>(),
+                                                  tets_b.as<tv_tet>(), verts_b.as<uint4>(), stats_b.as<Stats>(), E,
+                                                  flags_b.as<uint8_t>(), d_ctr);
+        CK(cudaGetLastError(), "eval");
+        TRY(select_flagged(fresh_b.as<uint32_t>(), n_fresh, F_MARK, marked_b, n_marked, false));
+        if (n_marked == 0) break;
+        crit += n_marked;
+        ++rounds;
+        // ---- closure ----
+        while (n_marked) {
+            TRY(grow_tets(static_cast<size_t>(n_t) + 2ull * n_marked));
+            TRY(grow_verts(static_cast<size_t>(n_v) + n_marked));
+            TRY(ensure(mid_b, n_marked * sizeof(uint32_t)));
+            TRY(ensure(miss_hi_b, n_marked * sizeof(uint64_t)));
+            TRY(ensure(miss_lo_b, n_marked * sizeof(uint32_t)));
+            TRY(ensure(miss_idx_b, n_marked * sizeof(uint32_t)));
+            TRY(ensure(miss_hi2_b, n_marked * sizeof(uint64_t)));
+            TRY(ensure(miss_lo2_b, n_marked * sizeof(uint32_t)));
+            TRY(ensure(miss_idx2_b, n_marked * sizeof(uint32_t)));
+            TRY(ensure(head_b, n_marked * sizeof(uint32_t)));
+            TRY(ensure(scan_b, n_marked * sizeof(uint32_t)));
+            CK(cudaMemset(d_cnt, 0, sizeof(uint32_t)), "memset");
+            midpoint_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, tets_b.as<tv_tet>(),
+                                                     verts_b.as<uint4>(), table_b.as<uint32_t>(), hmask,
+                                                     mid_b.as<uint32_t>(), miss_hi_b.as<uint64_t>(),
+                                                     miss_lo_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(), d_cnt, d_err);
+            CK(cudaGetLastError(), "midpoints");
+            uint32_t n_miss = 0;
+            CK(cudaMemcpy(&n_miss, d_cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost), "miss count");
+            if (n_miss) {
+                // stable LSD: by z, then by (x, y); payload = marked index
+                size_t tb1 = 0, tb2 = 0, tb3 = 0;
+                CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, miss_lo_b.as<uint32_t>(), miss_lo2_b.as<uint32_t>(),
+                                                   miss_idx_b.as<uint32_t>(), miss_idx2_b.as<uint32_t>(),
+                                                   static_cast<int>(n_miss), 0, 25),
+                   "sort sizing");
+                CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, miss_hi_b.as<uint64_t>(), miss_hi2_b.as<uint64_t>(),
+                                                   miss_idx2_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(),
+                                                   static_cast<int>(n_miss), 0, 50),
+                   "sort sizing");
+                CK(cub::DeviceScan::InclusiveSum(nullptr, tb3, head_b.as<uint32_t>(), scan_b.as<uint32_t>(),
+                                                 static_cast<int>(n_miss)),
+                   "scan sizing");
+                TRY(ensure(tmp_b, std::max(tb1, std::max(tb2, tb3))));
+                CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb1, miss_lo_b.as<uint32_t>(), miss_lo2_b.as<uint32_t>(),
+                                                   miss_idx_b.as<uint32_t>(), miss_idx2_b.as<uint32_t>(),
+                                                   static_cast<int>(n_miss), 0, 25),
+                   "sort lo");
+                // recompute the keys in z-sorted order (position p <- marked[idx2[p]])
+                regather_kernel<<<nblk(n_miss), 256>>>(miss_idx2_b.as<uint32_t>(), marked_b.as<uint32_t>(), n_miss,
+                                                       tets_b.as<tv_tet>(), verts_b.as<uint4>(),
+                                                       miss_hi_b.as<uint64_t>(), miss_lo_b.as<uint32_t>());
+                CK(cudaGetLastError(), "regather");
+                CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb2, miss_hi_b.as<uint64_t>(), miss_hi2_b.as<uint64_t>(),
+                                                   miss_idx2_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(),
+                                                   static_cast<int>(n_miss), 0, 50),
+                   "sort hi");
+                regather_kernel<<<nblk(n_miss), 256>>>(miss_idx_b.as<uint32_t>(), marked_b.as<uint32_t>(), n_miss,
+                                                       tets_b.as<tv_tet>(), verts_b.as<uint4>(),
+                                                       miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>());
+                CK(cudaGetLastError(), "regather");
+                dedup_heads_kernel<<<nblk(n_miss), 256>>>(miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>(), n_miss,
+                                                          head_b.as<uint32_t>());
+                CK(cub::DeviceScan::InclusiveSum(tmp_b.p, tb3, head_b.as<uint32_t>(), scan_b.as<uint32_t>(),
+                                                 static_cast<int>(n_miss)),
+                   "scan");
+                uint32_t n_new = 0;
+                CK(cudaMemcpy(&n_new, scan_b.as<uint32_t>() + n_miss - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost),
+                   "new verts");
+                TRY(grow_verts(static_cast<size_t>(n_v) + n_new));
+                dedup_assign_kernel<<<nblk(n_miss), 256>>>(miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>(),
+                                                           miss_idx_b.as<uint32_t>(), head_b.as<uint32_t>(),
+                                                           scan_b.as<uint32_t>(), n_miss, n_v, verts_b.as<uint4>(),
+                                                           table_b.as<uint32_t>(), hmask, mid_b.as<uint32_t>());
+                CK(cudaGetLastError(), "dedup assign");
+                n_v += n_new;
+            }
+            CK(cudaMemset(vtouch_b.p, 0, n_v), "vtouch");
+            bisect_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, n_t, tets_b.as<tv_tet>(),
+                                                   verts_b.as<uint4>(), mid_b.as<uint32_t>(), split_b.as<NodeRec>(),
+                                                   flags_b.as<uint8_t>(), vtouch_b.as<uint8_t>(), grid_max_level, d_err);
+            CK(cudaGetLastError(), "bisect");
+            n_t += 2 * n_marked;
+            bisections += n_marked;
+            ++passes;
+            CK(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost), "err");
+            if (herr) break;
+            // leaf list, hanging test
+            TRY(select_flagged(nullptr, n_t, F_LEAF, leaves_b, n_leaves, true));
+            CK(cudaMemset(d_cnt, 0, sizeof(uint32_t)), "memset");
+            hanging_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, tets_b.as<tv_tet>(),
+                                                    verts_b.as<uint4>(), table_b.as<uint32_t>(), hmask,
+                                                    vtouch_b.as<uint8_t>(), flags_b.as<uint8_t>(), d_cnt);
+            CK(cudaGetLastError(), "hanging");
+            TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_MARK, marked_b, n_marked, false));
+            clear_flag_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, flags_b.as<uint8_t>(), F_MARK);
+            CK(cudaGetLastError(), "clear");
+        }
+        if (herr) break;
+        // fresh = leaves created in this round
+        TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_NEW, fresh_b, n_fresh, false));
+    }
+    if (herr) {
+        if (herr & E_LEVEL) return set_error(TV_ERR_GRID, "bisect: level cap reached");
+        if (herr & E_MIDPOINT) return set_error(TV_ERR_GRID, "bisect: midpoint not representable");
+        if (herr & E_NORMAL) return set_error(TV_ERR_GRID, "normal direction not in table");
+        return set_error(TV_ERR_GRID, "build failed");
+    }
+
+    // ---- payloads for every leaf (builder.cpp:164-182) ----
+    TRY(select_flagged(nullptr, n_t, F_LEAF, leaves_b, n_leaves, true));
+    owner_descend_kernel<<<148 * 8, 256>>>(split_b.as<NodeRec>(), tets_b.as<tv_tet>(), nx, ny, nz,
+                                           owner_b.as<uint32_t>());
+    stats_zero_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, stats_b.as<Stats>(),
+                                               flags_b.as<uint8_t>());
+    stats_accum_kernel<<<148 * 8, 256>>>(V, owner_b.as<uint32_t>(), flags_b.as<uint8_t>(), stats_b.as<Stats>(), 1);
+    PayloadParams PP{cfg->density_scale, temp != nullptr, alb != nullptr};
+    payload_kernel<<<nblk(n_leaves, 128), 128>>>(leaves_b.as<uint32_t>(), n_leaves, V, owner_b.as<uint32_t>(),
+                                                 tets_b.as<tv_tet>(), verts_b.as<uint4>(), stats_b.as<Stats>(), PP,
+                                                 d_ctr, d_depth);
+    CK(cudaGetLastError(), "payloads");
+
+    // ---- neighbour links by face pairing (tet_grid.cpp:130-152) ----
+    {
+        const uint64_t nf = 4ull * n_leaves;
+        Buf khi, klo, rec, khi2, klo2, rec2;
+        TRY(ensure(khi, nf * 8));
+        TRY(ensure(klo, nf * 4));
+        TRY(ensure(rec, nf * 4));
+        TRY(ensure(khi2, nf * 8));
+        TRY(ensure(klo2, nf * 4));
+        TRY(ensure(rec2, nf * 4));
+        face_keys_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, tets_b.as<tv_tet>(),
+                                                  khi.as<uint64_t>(), klo.as<uint32_t>(), rec.as<uint32_t>());
+        CK(cudaGetLastError(), "face keys");
+        size_t tb1 = 0, tb2 = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, klo.as<uint32_t>(), klo2.as<uint32_t>(), rec.as<uint32_t>(),
+                                           rec2.as<uint32_t>(), static_cast<int>(nf)),
+           "sort sizing");
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, khi.as<uint64_t>(), khi2.as<uint64_t>(), rec2.as<uint32_t>(),
+                                           rec.as<uint32_t>(), static_cast<int>(nf)),
+           "sort sizing");
+        TRY(ensure(tmp_b, std::max(tb1, tb2)));
+        // sort by v2, gather v0v1 in that order, then stable sort by v0v1
+        CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb1, klo.as<uint32_t>(), klo2.as<uint32_t>(), rec.as<uint32_t>(),
+                                           rec2.as<uint32_t>(), static_cast<int>(nf)),
+           "face sort lo");
+        gather_face_hi_kernel<<<nblk(nf), 256>>>(rec2.as<uint32_t>(), nf, leaves_b.as<uint32_t>(), tets_b.as<tv_tet>(),
+                                                 khi.as<uint64_t>(), klo.as<uint32_t>());
+        CK(cudaGetLastError(), "face gather");
+        CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb2, khi.as<uint64_t>(), khi2.as<uint64_t>(), rec2.as<uint32_t>(),
+                                           rec.as<uint32_t>(), static_cast<int>(nf)),
+           "face sort hi");
+        gather_face_hi_kernel<<<nblk(nf), 256>>>(rec.as<uint32_t>(), nf, leaves_b.as<uint32_t>(), tets_b.as<tv_tet>(),
+                                                 khi2.as<uint64_t>(), klo2.as<uint32_t>());
+        face_pair_kernel<<<nblk(nf), 256>>>(khi2.as<uint64_t>(), klo2.as<uint32_t>(), rec.as<uint32_t>(), nf,
+                                            leaves_b.as<uint32_t>(), tets_b.as<tv_tet>(), d_err);
+        CK(cudaGetLastError(), "face pair");
+    }
+    CK(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost), "err");
+    if (herr & E_FACE) return set_error(TV_ERR_GRID, "face shared by more than two leaves");
+    unsigned long long hctr[2] = {0, 0};
+    CK(cudaMemcpy(hctr, d_ctr, sizeof(hctr), cudaMemcpyDeviceToHost), "counters");
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+
+    // ---- hand the pools to the traversal layout ----
+    auto h = new tv_grid();
+    DeviceGrid& g = h->g;
+    g.device = device;
+    g.n_vertices = n_v;
+    g.n_tets = n_t;
+    g.n_leaves = n_leaves;
+    g.n_internal = n_t - n_leaves;
+    g.max_level = grid_max_level;
+    std::memcpy(g.roots, roots, sizeof(roots));
+    cudaError_t e = cudaMalloc(&g.tets, static_cast<size_t>(n_t) * sizeof(tv_tet));
+    if (e == cudaSuccess) e = cudaMalloc(&g.verts, static_cast<size_t>(n_v) * sizeof(uint4));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g.tets, tets_b.p, static_cast<size_t>(n_t) * sizeof(tv_tet), cudaMemcpyDeviceToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g.verts, verts_b.p, static_cast<size_t>(n_v) * sizeof(uint4), cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) {
+        free_grid(g);
+        delete h;
+        return cuda_status(e, "build output");
+    }
+    g.bytes = static_cast<uint64_t>(n_t) * sizeof(tv_tet) + static_cast<uint64_t>(n_v) * sizeof(uint4);
+    rc = finalize_grid(g, nullptr);
+    if (rc) {
+        free_grid(g);
+        delete h;
+        return rc;
+    }
+    if (stats) {
+        stats->leaf_count = n_leaves;
+        stats->max_depth = g.max_depth;
+        stats->rounds = rounds;
+        stats->seconds = ms * 1e-3;
+        stats->criterion_splits = crit;
+        stats->propagation_splits = bisections - crit;
+        stats->closure_passes = passes;
+        stats->voxel_visits = hctr[1];
+    }
+    (void)replays;
+    *out = h;
+    return TV_OK;
+#undef CK
+#undef TRY
+}
+
 }  // namespace tvb
 
 using namespace tvb;
@@ -79,16 +1302,42 @@ int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, dou
     return cuda_status(e, "generate volume");
 }
 
-int tv_build_dev(const float*, const float*, const float*, int32_t, int32_t, int32_t, const tv_build_config*,
-                 const tv_camera*, int, tv_grid** out, tv_build_stats*) {
-    if (out) *out = nullptr;
-    return set_error(TV_ERR, "tv_build_dev: GPU LEB build not available in this build");
+int tv_build_dev(const float* density_dev, const float* temperature_dev, const float* albedo_dev, int32_t nx,
+                 int32_t ny, int32_t nz, const tv_build_config* cfg, const tv_camera* camera, int device,
+                 tv_grid** out, tv_build_stats* stats) {
+    if (!out || !density_dev) return set_error(TV_ERR_ARG, "null argument");
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return set_error(TV_ERR_CUDA, "no CUDA device available");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+    return build_grid(density_dev, temperature_dev, albedo_dev, nx, ny, nz, cfg, camera, device, out, stats);
 }
 
-int tv_build(const float*, const float*, const float*, int32_t, int32_t, int32_t, const tv_build_config*,
-             const tv_camera*, int, tv_grid** out, tv_build_stats*) {
-    if (out) *out = nullptr;
-    return set_error(TV_ERR, "tv_build: GPU LEB build not available in this build");
+int tv_build(const float* density, const float* temperature, const float* albedo, int32_t nx, int32_t ny,
+             int32_t nz, const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out,
+             tv_build_stats* stats) {
+    if (!out || !density) return set_error(TV_ERR_ARG, "null argument");
+    *out = nullptr;
+    if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR_CONFIG, "volume dimensions must be positive");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return set_error(TV_ERR_CUDA, "no CUDA device available");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_status(e, "cudaSetDevice");
+    const size_t nv = static_cast<size_t>(nx) * ny * nz * sizeof(float);
+    float *d = nullptr, *t = nullptr, *a = nullptr;
+    e = cudaMalloc(&d, nv);
+    if (e == cudaSuccess && temperature) e = cudaMalloc(&t, nv);
+    if (e == cudaSuccess && albedo) e = cudaMalloc(&a, nv);
+    if (e == cudaSuccess) e = cudaMemcpy(d, density, nv, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && t) e = cudaMemcpy(t, temperature, nv, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && a) e = cudaMemcpy(a, albedo, nv, cudaMemcpyHostToDevice);
+    int rc = e == cudaSuccess ? build_grid(d, t, a, nx, ny, nz, cfg, camera, device, out, stats)
+                              : cuda_status(e, "volume upload");
+    cudaFree(d);
+    cudaFree(t);
+    cudaFree(a);
+    return rc;
 }
 
 int tv_render_regular(const float*, int32_t, int32_t, int32_t, double, const tv_camera*, const tv_render_config*, int,

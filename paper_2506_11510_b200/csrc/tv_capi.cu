@@ -38,8 +38,10 @@ namespace {
         if (rc_) return rc_;                            \
     } while (0)
 
+}  // namespace
+
 // camera.cpp:12-45 (host; std::tan runs here, never on the device)
-int make_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]) {
+int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]) {
     if (!c) return set_error(TV_ERR_ARG, "camera is null");
     if (c->width < 1 || c->height < 1) return set_error(TV_ERR_CAMERA, "image dimensions must be positive");
     if (!(c->vfov_degrees > 0.0 && c->vfov_degrees < 180.0))
@@ -80,6 +82,8 @@ int make_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]) {
     }
     return TV_OK;
 }
+
+namespace {
 
 // RenderConfig::validate (tracer.cpp:131-141)
 int validate_render(const tv_render_config* r) {
@@ -311,7 +315,7 @@ int tv_render(const tv_grid* h, const tv_camera* camera, const tv_render_config*
     int rc = validate_render(cfg);
     if (rc) return rc;
     CamView cv;
-    if ((rc = make_camera(camera, cv, nullptr, nullptr))) return rc;
+    if ((rc = host_camera(camera, cv, nullptr, nullptr))) return rc;
     const DeviceGrid& g = h->g;
     if ((rc = use_device(g.device))) return rc;
     const uint64_t npx = static_cast<uint64_t>(cv.w) * cv.h;
@@ -360,7 +364,7 @@ int tv_render_tiles(const tv_grid* h, const tv_camera* camera, const tv_render_c
     int rc = validate_render(cfg);
     if (rc) return rc;
     CamView cv;
-    if ((rc = make_camera(camera, cv, nullptr, nullptr))) return rc;
+    if ((rc = host_camera(camera, cv, nullptr, nullptr))) return rc;
     const DeviceGrid& g = h->g;
     if ((rc = use_device(g.device))) return rc;
     // per-(device, thread) work counter

@@ -1,0 +1,129 @@
+"""GPU LEB build parity: tv_build against build_adaptive_grid (builder.cpp:118-182).
+
+Tet and vertex ids are allocation-order artefacts, so parity is
+on the canonical leaf set: every leaf as its sorted four fixed-point corners,
+plus the f32 bit patterns of its payload and its mask — bit-exact. The
+downloaded GPU grid must also pass the reference's own TetGrid::validate()
+(conformity, reciprocal neighbour links, canonical normals, exact volume), and
+render bit-identically to the oracle-built grid.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tv():
+    import paper_2506_11510_b200 as tv
+
+    assert tv.device_count() >= 1, "no CUDA device: the product has no CPU fallback"
+    return tv
+
+
+def canonical(vq, tets):
+    leaf = tets["children"][:, 0] == O.NO_TET
+    t = tets[leaf]
+    corners = vq[t["verts"]]  # (L, 4, 3)
+    order = np.lexsort((corners[:, :, 2], corners[:, :, 1], corners[:, :, 0]), axis=1)
+    corners = np.take_along_axis(corners, order[:, :, None], axis=1).reshape(len(t), 12)
+    pay = np.stack([t["density"].view(np.uint32), t["temperature"].view(np.uint32), t["albedo"].view(np.uint32),
+                    t["mask"].astype(np.uint32), t["level"].astype(np.uint32)], axis=1)
+    rows = np.concatenate([corners.astype(np.uint64), pay.astype(np.uint64)], axis=1)
+    idx = np.lexsort(rows.T[::-1])
+    return rows[idx]
+
+
+def gpu_build(tv, vol, bc, cam=None, temperature=None, albedo=None):
+    tb = tv.BuildConfig(bc.variation_threshold, bc.max_level, bool(bc.use_camera), bc.pixel_threshold,
+                        bc.density_scale)
+    tcam = None
+    if cam is not None:
+        tcam = tv.PinholeCamera(tuple(cam.pos), tuple(cam.fwd), tuple(cam.up), cam.vfov, cam.width, cam.height)
+    return tv.build_adaptive_grid(vol, tb, tcam, temperature=temperature, albedo=albedo)
+
+
+def check_same(tv, vol, bc, cam=None, temperature=None, albedo=None, validate=True):
+    og, ost = O.build(O.c_oracle(), vol, bc, cam, temperature, albedo)
+    dg, dst = gpu_build(tv, vol, bc, cam, temperature, albedo)
+    v, t, r = dg.download()
+    p = og.pools()
+    assert dst.leaf_count == ost["leaf_count"]
+    assert dst.max_depth == ost["max_depth"]
+    assert len(t) == len(p.tets) and len(v) == len(p.vq)
+    a, b = canonical(p.vq, p.tets), canonical(v, t.view(O.TET_DTYPE))
+    assert np.array_equal(a, b), "canonical leaf set / payload bits differ"
+    # total bisections are order independent; the criterion/propagation split is reported
+    assert dst.criterion_splits + dst.propagation_splits == ost["criterion_splits"] + ost["propagation_splits"]
+    ref = O.ref_oracle()
+    if validate and ref is not None:
+        pools = O.Pools(v, t.view(O.TET_DTYPE), r, 48)
+        rg = O.from_pools(ref, pools)
+        msg = O.C.create_string_buffer(256)
+        out = np.zeros(3, np.uint64)
+        ok = ref.fn("grid_validate")(rg.h, msg, 256, out.ctypes.data_as(O._U64))
+        assert ok == 1, msg.value.decode()
+    return og, ost, dg, dst
+
+
+def test_build_c1_blob(tv):
+    vol = O.gen_volume("blob", 64)
+    og, ost, dg, dst = check_same(tv, vol, O.build_cfg(0.15, 12, False, 1.0, 8.0))
+    assert dst.leaf_count == 51020
+    # the GPU-built grid renders bit-identically (golden C1 hash)
+    img = tv.render(dg, tv.PinholeCamera((0.5, 0.5, -2), (0, 0, 1), (0, 1, 0), 40, 256, 256),
+                    tv.RenderConfig(spp=4, max_bounces=2, seed=0))
+    assert img.cells_visited == 4612915
+    assert O.fnv64(img.sum) == 0x5DD59BA4FB717D7F
+
+
+def test_build_constant_stays_at_roots(tv):
+    """test_builder.cpp:53-72"""
+    vol = O.gen_volume("constant", 8, 1.0)
+    _, _, dg, dst = check_same(tv, vol, O.build_cfg(0.1, 10, False, 1.0, 2.5))
+    assert dst.leaf_count == 24 and dst.max_depth == 0 and dst.criterion_splits == 0
+    _, t, _ = dg.download()
+    assert np.all(t["density"] == np.float32(2.5)) and np.all(t["mask"] == 1)
+
+
+def test_build_step_noise_ramp(tv):
+    for kind, n, thr, ml, sc in [("step", 16, 0.5, 6, 1.0), ("noise", 24, 0.2, 10, 3.0), ("ramp", 12, 0.05, 8, 1.0),
+                                 ("step", 33, 0.3, 15, 4.0)]:
+        check_same(tv, O.gen_volume(kind, n), O.build_cfg(thr, ml, False, 1.0, sc))
+
+
+def test_build_camera_criterion_acceptance11(tv):
+    cam = O.camera((0.5, 0.5, -2), (0, 0, 1), (0, 1, 0), 16, 128, 128)
+    _, _, _, dst = check_same(tv, O.gen_volume("blob", 32), O.build_cfg(0.15, 9, True, 0.5, 1.0), cam)
+    assert dst.leaf_count == 7528
+
+
+def test_build_cloud64_camera(tv):
+    """cloud64 + camera -> 361,510 leaves."""
+    cam = O.camera((0.5, 0.5, -1.2), (0, 0, 1), (0, 1, 0), 40, 1024, 1024)
+    _, _, _, dst = check_same(tv, O.gen_volume("cloud", 64), O.build_cfg(0.15, 18, True, 1.0, 16.0), cam)
+    assert dst.leaf_count == 361510
+
+
+def test_build_with_temperature_and_albedo(tv):
+    vol = O.gen_volume("noise", 20)
+    temp = np.clip(vol, 0, 1).astype(np.float32)
+    alb = (0.3 + 0.5 * O.gen_volume("ramp", 20)).astype(np.float32)
+    check_same(tv, vol, O.build_cfg(0.1, 9, False, 1.0, 5.0), None, temp, alb)
+
+
+def test_build_nonuniform_dims(tv):
+    vol = np.ascontiguousarray(O.gen_volume("cloud", 48)[:, 5:37, 3:43])  # (48, 32, 40)
+    check_same(tv, vol, O.build_cfg(0.3, 14, False, 1.0, 8.0))
+
+
+def test_build_config_errors(tv):
+    vol = O.gen_volume("blob", 8)
+    with pytest.raises(tv.ConfigError, match="variationThreshold"):
+        tv.build_adaptive_grid(vol, tv.BuildConfig(variation_threshold=-1.0))
+    with pytest.raises(tv.ConfigError, match="maxLevel"):
+        tv.build_adaptive_grid(vol, tv.BuildConfig(max_level=49))
+    with pytest.raises(tv.ConfigError, match="useCamera"):
+        tv.build_adaptive_grid(vol, tv.BuildConfig(use_camera=True))
