@@ -1,0 +1,355 @@
+"""Benchmark: BASELINE.json metric on config C2.
+
+Workload (one "step" = one frame): procedural cloud 256^3 -> LEB tet grid built
+on the GPU with the camera criterion (threshold 0.15, max_level 24,
+density_scale 16, pixel_threshold 1) -> 1024x1024 render at 32 spp,
+max_bounces 64, camera (0.5, 0.5, -1.2) looking +z, vfov 40. The grid (12.1M
+leaves, 3.3 GB in HBM) is resident before timing; it is larger than L2, which
+is how this benchmark satisfies the L2 rule (no flush between steps).
+
+With --gpus N (torchrun, one rank per GPU) every rank holds a replica of the
+grid and renders the interleaved 16x16 tiles t with t % N == rank of the SAME
+frame (strong scaling); the tiles are packed and all-gathered over NCCL and
+unpacked into the full frame on every rank, inside the timed step.
+
+--impl reference times the reference's own CPU renderer (oracle/_ref, compiled
+from /root/reference) on this box's host cores on a bounded sample of the same
+workload (the first sample of every pixel of the same frame: spp = 1).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+W_IMG = H_IMG = 1024
+SPP = 32
+GRID_N = 256
+BUILD = dict(variation_threshold=0.15, max_level=24, use_camera=True, pixel_threshold=1.0, density_scale=16.0)
+CAM = dict(position=(0.5, 0.5, -1.2), forward=(0.0, 0.0, 1.0), up=(0.0, 1.0, 0.0), vfov_degrees=40.0, width=W_IMG,
+           height=H_IMG)
+BYTES_PER_STEP = 64  # 48 B leaf record + 16 B vertex per tet-step
+WORKLOAD = ("C2: procedural cloud 256^3 -> GPU LEB grid (camera criterion, threshold 0.15, max_level 24, "
+            "density_scale 16, pixel_threshold 1) -> 1024x1024 x 32 spp, max_bounces 64")
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_render_sample(v, t, r, max_level, threads=0):
+    """The reference renderer (oracle/_ref) on the same grid and frame, spp = 1."""
+    import oracle as O
+
+    chk = O.ref_oracle()
+    kind = "reference"
+    if chk is None:
+        chk, kind = O.c_oracle(), "port"
+    g = O.from_pools(chk, O.Pools(v, t.view(O.TET_DTYPE), r, max_level))
+    cam = O.camera(CAM["position"], CAM["forward"], CAM["up"], CAM["vfov_degrees"], W_IMG, H_IMG)
+    rc = O.render_cfg(spp=1, max_bounces=64, seed=0)
+    out = g.render(cam, rc, threads)
+    cores = threads if threads > 0 else os.cpu_count()
+    return out, kind, cores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU renderer on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import paper_2506_11510_b200 as tv  # grid construction only (reference arm)
+    import torch
+
+    torch.cuda.set_device(0)
+    vol = torch.empty(GRID_N ** 3, dtype=torch.float32, device="cuda")
+    tv.generate_volume_dev("cloud", GRID_N, vol.data_ptr())
+    grid, bst = tv.build_adaptive_grid_dev(vol.data_ptr(), (GRID_N,) * 3, tv.BuildConfig(**BUILD),
+                                           tv.PinholeCamera(**CAM))
+    v, t, r = grid.download()
+    grid.close()
+    del vol
+    import oracle as O
+
+    chk = O.ref_oracle()
+    kind = "reference" if chk is not None else "port"
+    chk = chk or O.c_oracle()
+    t0 = time.time()
+    g = O.from_pools(chk, O.Pools(v, t.view(O.TET_DTYPE), r, BUILD["max_level"]))
+    assemble_s = time.time() - t0
+    cam = O.camera(CAM["position"], CAM["forward"], CAM["up"], CAM["vfov_degrees"], W_IMG, H_IMG)
+    rc = O.render_cfg(spp=1, max_bounces=64, seed=0)
+    for _ in range(args.warmup):
+        g.render(cam, rc, 0)
+    secs, cells = [], 0
+    for _ in range(args.steps):
+        out = g.render(cam, rc, 0)
+        secs.append(out["seconds"])
+        cells = out["cells_visited"]
+    per = float(np.mean(secs))
+    samples = W_IMG * H_IMG
+    value = samples / per
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": "samples/s", "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": "spp=1 of the same frame (first sample of every pixel)",
+                   "leaves": int((t["children"][:, 0] == 0xFFFFFFFF).sum())},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
+                         "sample": "1024x1024 x 1 spp of the C2 frame, all host threads (render(..., threads=0))"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "tet_steps_per_s": cells / per, "cells_per_path": cells / samples,
+        "grid_assemble_s": assemble_s, "cpu_model": _cpu_model(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_11510_b200 as tv
+    from paper_2506_11510_b200 import sharding
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+
+    # ---- grid: generated and built in HBM (not timed) ----
+    vol = torch.empty(GRID_N ** 3, dtype=torch.float32, device="cuda")
+    tv.generate_volume_dev("cloud", GRID_N, vol.data_ptr(), device=dev)
+    cam = tv.PinholeCamera(**CAM)
+    grid, bst = tv.build_adaptive_grid_dev(vol.data_ptr(), (GRID_N,) * 3, tv.BuildConfig(**BUILD), cam, device=dev)
+    del vol
+    info = grid.info()
+    rc = tv.RenderConfig(spp=SPP, max_bounces=64, seed=0)
+
+    npx = W_IMG * H_IMG
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    sum_ = torch.zeros(npx * 3, dtype=torch.float64, device="cuda")
+    sum_sq = torch.zeros(npx * 3, dtype=torch.float64, device="cuda")
+    counts = torch.zeros(npx, dtype=torch.int32, device="cuda")
+    stats = torch.zeros(3, dtype=torch.int64, device="cuda")
+    words = tv.tile_pack_words(W_IMG, H_IMG, rank, world, 3)
+    packed = torch.zeros(words, dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(words * world, dtype=torch.float64, device="cuda")
+    launches_per_step = 1 + (2 + world if world > 1 else 0)
+    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def step(i, timed=False):
+        if timed:
+            k_start[i].record(stream)
+        tv.render_tiles(grid, cam, rc, rank, world, sum_.data_ptr(), sum_sq.data_ptr(), counts.data_ptr(),
+                        stats.data_ptr(), sh)
+        if timed:
+            k_end[i].record(stream)
+        if world > 1:
+            tv.tile_pack(sum_.data_ptr(), packed.data_ptr(), W_IMG, H_IMG, rank, world, 3, sh)
+            with torch.cuda.stream(stream):
+                dist.all_gather_into_tensor(gathered, packed)
+            for r in range(world):
+                tv.tile_unpack(gathered[r * words:(r + 1) * words].data_ptr(), sum_.data_ptr(), W_IMG, H_IMG, r,
+                               world, 3, sh)
+
+    for i in range(args.warmup):
+        step(i)
+    stream.synchronize()
+    stats.zero_()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i, timed=True)
+        t1.record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    kern_ms = float(np.mean([k_start[i].elapsed_time(k_end[i]) for i in range(args.steps)]))
+    st = stats.cpu().numpy()
+    cells_rank = int(st[0]) // args.steps
+    if world > 1:
+        red = torch.tensor([ms, kern_ms, float(cells_rank)], dtype=torch.float64, device="cuda")
+        mx = red.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = red.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        ms, kern_ms_max = float(mx[0]), float(mx[1])
+        cells_frame = int(tot[2])
+    else:
+        kern_ms_max = kern_ms
+        cells_frame = cells_rank
+    samples = npx * SPP
+    value = samples / (ms * 1e-3)
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if world == 1:
+        hs = torch.empty(npx * 3, dtype=torch.float64, pin_memory=True).numpy()
+        hq = torch.empty(npx * 3, dtype=torch.float64, pin_memory=True).numpy()
+        hc = torch.empty(npx, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        tv.render_into(grid, cam, rc, hs, hq, hc)
+        t_e = time.perf_counter()
+        for _ in range(args.steps):
+            tv.render_into(grid, cam, rc, hs, hq, hc)
+        e2e_s = (time.perf_counter() - t_e) / args.steps
+        e2e = {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": 96 + 88,
+               "d2h_bytes_per_step": npx * (24 + 24 + 4) + 24, "ms_per_step": e2e_s * 1e3,
+               "path": "tv_render (C ABI): kernel params H2D, sum/sum_sq/sample_counts D2H into pinned host memory"}
+    else:
+        host = torch.empty(npx * 3, dtype=torch.float64, pin_memory=True)
+        for i in range(2):
+            step(0)
+        stream.synchronize()
+        dist.barrier()
+        t_e = time.perf_counter()
+        for i in range(args.steps):
+            step(0)
+            if rank == 0:
+                with torch.cuda.stream(stream):
+                    host.copy_(sum_, non_blocking=True)
+            stream.synchronize()
+        e2e_s = (time.perf_counter() - t_e) / args.steps
+        e2 = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(e2, op=dist.ReduceOp.MAX)
+        e2e_s = float(e2[0])
+        e2e = {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": 96 + 88,
+               "d2h_bytes_per_step": npx * 24, "ms_per_step": e2e_s * 1e3,
+               "path": "tv_render_tiles + NCCL all-gather of packed tiles + D2H of the frame sums on rank 0"}
+
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    achieved = cells_rank * BYTES_PER_STEP / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "render_kernel_dram.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "kernel": "render_kernel", "kernel_ms": kern_ms,
+                "bytes_per_step": BYTES_PER_STEP, "tet_steps_per_launch": cells_rank,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, t, r = grid.download()
+            out, kind, cores = cpu_render_sample(v, t, r, BUILD["max_level"])
+            cpu = {"value": npx / out["seconds"], "unit": "samples/s", "cores": cores, "kind": kind,
+                   "sample": "1024x1024 x 1 spp of the same C2 frame (first sample per pixel), threads=all",
+                   "seconds": out["seconds"], "tet_steps_per_s": out["cells_visited"] / out["seconds"]}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": "failed", "error": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": "samples/s", "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (procedural cloud field, GPU-built LEB grid)",
+            "config": {"workload": WORKLOAD, "leaves": info["n_leaves"], "tets": info["n_tets"],
+                       "grid_bytes": info["device_bytes"], "max_depth": info["max_depth"],
+                       "l2": "inputs larger than L2 (3.3 GB grid), no flush", "parallelism": f"image tiles x{world}",
+                       "build_s_device": bst.seconds},
+            "tet_steps_per_s": cells_frame / (ms * 1e-3), "cells_per_path": cells_frame / samples,
+            "ms_per_frame": ms, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
