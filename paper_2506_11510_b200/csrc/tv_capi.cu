@@ -122,70 +122,92 @@ int use_device(int device) {
     return cuda_status(cudaSetDevice(device), "cudaSetDevice");
 }
 
-int render_blocks(int device) {
-    static std::mutex mu;
-    static int cached[64] = {0};
-    std::lock_guard<std::mutex> lk(mu);
-    if (device >= 0 && device < 64 && cached[device]) return cached[device];
-    int sms = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_kernel, kRenderThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    const int b = sms * per_sm;
-    if (device >= 0 && device < 64) cached[device] = b;
-    return b;
+// Per-device workspace reused across frames (no cudaMalloc in the per-frame
+// path): the per-path buffers of a batch (start records, entry cells,
+// radiance), the accumulators tv_render copies back, the queue counter, and a
+// stream + events. One frame is in flight per device at a time.
+struct Workspace {
+    std::mutex mu;
+    void* paths = nullptr;
+    size_t path_bytes = 0;
+    void* out = nullptr;
+    size_t out_bytes = 0;
+    uint32_t* counter = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int trace_blocks = 0, sms = 0;
+};
+Workspace g_ws[64];
+
+int grow(void*& p, size_t& have, size_t need) {
+    if (have >= need) return TV_OK;
+    cudaFree(p);
+    p = nullptr;
+    have = 0;
+    TV_CK(cudaMalloc(&p, need), "workspace alloc");
+    have = need;
+    return TV_OK;
 }
 
-// Launches the persistent render kernel over this rank's tiles.
-int launch_render(const DeviceGrid& g, const CamView& cv, const RenderParams& rp, int rank, int n_ranks,
-                  RenderOut out, uint32_t* counter, cudaStream_t st) {
+int workspace(int device, Workspace*& out) {
+    if (device < 0 || device >= 64) return set_error(TV_ERR_ARG, "device index out of range");
+    Workspace& w = g_ws[device];
+    if (!w.stream) {
+        TV_CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking), "stream create");
+        TV_CK(cudaEventCreate(&w.ev0), "event create");
+        TV_CK(cudaEventCreate(&w.ev1), "event create");
+        TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
+        int per_sm = 1;
+        cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel, kTraceThreads, 0);
+        w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
+    }
+    out = &w;
+    return TV_OK;
+}
+
+// Renders this rank's tiles of one frame: per batch of samples, start ->
+// trace -> accumulate (see tv_trace.cu). Asynchronous on `st`.
+int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp, int rank, int n_ranks,
+                 RenderOut out, Workspace& w, cudaStream_t st) {
     const uint32_t tiles_x = (static_cast<uint32_t>(cv.w) + 15) / 16;
     const uint32_t tiles_y = (static_cast<uint32_t>(cv.h) + 15) / 16;
     const uint64_t tiles = static_cast<uint64_t>(tiles_x) * tiles_y;
     const uint64_t mine = tiles > static_cast<uint64_t>(rank) ? (tiles - rank + n_ranks - 1) / n_ranks : 0;
-    TileSched S;
-    S.counter = counter;
-    S.n_units = static_cast<uint32_t>(mine * 8);
-    S.tiles_x = tiles_x;
-    S.rank = rank;
-    S.n_ranks = n_ranks;
-    TV_CK(cudaMemsetAsync(counter, 0, sizeof(uint32_t), st), "memset counter");
-    const int nb = render_blocks(g.device);
-    const uint64_t need = (S.n_units + (kRenderThreads / 32) - 1) / (kRenderThreads / 32);
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nb, std::max<uint64_t>(need, 1)));
-    render_kernel<<<grid, kRenderThreads, 0, st>>>(g.view, cv, rp, S, out);
-    return cuda_status(cudaGetLastError(), "render_kernel launch");
-}
-
-// Per-device scratch reused across tv_render calls (avoids cudaMalloc in the
-// per-frame path).
-struct Scratch {
-    int device = -1;
-    size_t bytes = 0;
-    void* buf = nullptr;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-};
-std::mutex g_scratch_mu;
-Scratch g_scratch[64];
-
-int scratch_for(int device, size_t bytes, Scratch*& out) {
-    if (device < 0 || device >= 64) return set_error(TV_ERR_ARG, "device index out of range");
-    Scratch& s = g_scratch[device];
-    if (!s.stream) {
-        TV_CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "stream create");
-        TV_CK(cudaEventCreate(&s.ev0), "event create");
-        TV_CK(cudaEventCreate(&s.ev1), "event create");
+    const uint64_t units = mine * 8;
+    if (units == 0) return TV_OK;
+    uint64_t ns = std::max<uint64_t>(1, kMaxBatchPaths / (units * 32));
+    ns = std::min<uint64_t>(ns, static_cast<uint64_t>(rp.spp));
+    if (units * 32 * ns >= (1ull << 31)) return set_error(TV_ERR_ARG, "frame too large for one batch");
+    const uint64_t max_paths = units * 32 * ns;
+    const size_t need = max_paths * (sizeof(StartRec) + sizeof(uint32_t) + 3 * sizeof(double)) + 256;
+    int rc = grow(w.paths, w.path_bytes, need);
+    if (rc) return rc;
+    char* base = static_cast<char*>(w.paths);
+    StartRec* st_rec = reinterpret_cast<StartRec*>(base);
+    double* rad = reinterpret_cast<double*>(base + max_paths * sizeof(StartRec));
+    uint32_t* cells = reinterpret_cast<uint32_t*>(base + max_paths * (sizeof(StartRec) + 3 * sizeof(double)));
+    for (uint64_t s0 = 0; s0 < static_cast<uint64_t>(rp.spp); s0 += ns) {
+        Batch B;
+        B.n_units = static_cast<uint32_t>(units);
+        B.s0 = static_cast<uint32_t>(s0);
+        B.ns = static_cast<uint32_t>(std::min<uint64_t>(ns, rp.spp - s0));
+        B.tiles_x = tiles_x;
+        B.rank = rank;
+        B.n_ranks = n_ranks;
+        B.n_paths = static_cast<uint32_t>(units * 32 * B.ns);
+        B.first = s0 == 0 ? 1u : 0u;
+        const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
+        start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);
+        TV_CK(cudaGetLastError(), "start_kernel launch");
+        TV_CK(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), st), "memset counter");
+        trace_kernel<<<w.trace_blocks, kTraceThreads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
+                                                               w.counter);
+        TV_CK(cudaGetLastError(), "trace_kernel launch");
+        const unsigned ab = static_cast<unsigned>(std::min<uint64_t>((units * 32 + 127) / 128, w.sms * 16ull));
+        accum_kernel<<<ab, 128, 0, st>>>(B, cv, cells, rad, out);
+        TV_CK(cudaGetLastError(), "accum_kernel launch");
     }
-    if (s.bytes < bytes) {
-        cudaFree(s.buf);
-        s.buf = nullptr;
-        s.bytes = 0;
-        TV_CK(cudaMalloc(&s.buf, bytes), "scratch alloc");
-        s.bytes = bytes;
-    }
-    s.device = device;
-    out = &s;
     return TV_OK;
 }
 
@@ -319,20 +341,21 @@ int tv_render(const tv_grid* h, const tv_camera* camera, const tv_render_config*
     const DeviceGrid& g = h->g;
     if ((rc = use_device(g.device))) return rc;
     const uint64_t npx = static_cast<uint64_t>(cv.w) * cv.h;
+    Workspace* w;
+    if ((rc = workspace(g.device, w))) return rc;
+    std::lock_guard<std::mutex> lk(w->mu);
     const size_t bytes = npx * (3 * sizeof(double) * 2 + sizeof(uint32_t)) + 4 * sizeof(uint64_t) + 256;
-    std::lock_guard<std::mutex> lk(g_scratch_mu);
-    Scratch* s;
-    if ((rc = scratch_for(g.device, bytes, s))) return rc;
-    char* base = static_cast<char*>(s->buf);
+    if ((rc = grow(w->out, w->out_bytes, bytes))) return rc;
+    Workspace* s = w;
+    char* base = static_cast<char*>(w->out);
     double* sum = reinterpret_cast<double*>(base);
     double* sum_sq = sum + 3 * npx;
     uint32_t* counts = reinterpret_cast<uint32_t*>(sum_sq + 3 * npx);
     uint64_t* st = reinterpret_cast<uint64_t*>(base + ((npx * 48 + npx * 4 + 63) & ~static_cast<size_t>(63)));
-    uint32_t* counter = reinterpret_cast<uint32_t*>(st + 3);
     RenderOut ro{sum, sum_sq, counts, st};
     TV_CK(cudaMemsetAsync(st, 0, 3 * sizeof(uint64_t), s->stream), "memset stats");
     TV_CK(cudaEventRecord(s->ev0, s->stream), "event");
-    if ((rc = launch_render(g, cv, make_params(cfg), 0, 1, ro, counter, s->stream))) return rc;
+    if ((rc = render_frame(g, cv, make_params(cfg), 0, 1, ro, *w, s->stream))) return rc;
     TV_CK(cudaEventRecord(s->ev1, s->stream), "event");
     if (out && out->sum)
         TV_CK(cudaMemcpyAsync(out->sum, sum, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost, s->stream), "D2H");
@@ -367,12 +390,11 @@ int tv_render_tiles(const tv_grid* h, const tv_camera* camera, const tv_render_c
     if ((rc = host_camera(camera, cv, nullptr, nullptr))) return rc;
     const DeviceGrid& g = h->g;
     if ((rc = use_device(g.device))) return rc;
-    // per-(device, thread) work counter
-    thread_local uint32_t* counter[64] = {nullptr};
-    if (!counter[g.device]) TV_CK(cudaMalloc(&counter[g.device], 64), "counter alloc");
+    Workspace* w;
+    if ((rc = workspace(g.device, w))) return rc;
+    std::lock_guard<std::mutex> lk(w->mu);
     RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
-    return launch_render(g, cv, make_params(cfg), rank, n_ranks, ro, counter[g.device],
-                         static_cast<cudaStream_t>(stream));
+    return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream));
 }
 
 int tv_march_segments(const tv_grid* h, const tv_ray* rays, uint64_t n, tv_segment* out, uint64_t* offsets,

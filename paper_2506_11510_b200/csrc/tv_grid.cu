@@ -66,32 +66,26 @@ __device__ __forceinline__ uint32_t encode_child(uint32_t c, const tv_tet* tets,
 }
 
 __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* __restrict__ order,
-                              const uint32_t* __restrict__ tet2leaf, uint64_t n_leaves, LeafRec* out,
-                              int* max_depth) {
+                              const uint32_t* __restrict__ tet2leaf, const uint4* __restrict__ verts,
+                              uint64_t n_leaves, LeafRec* out, uint8_t* mask, int* max_depth) {
     const uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (L >= n_leaves) return;
     const tv_tet tt = tets[order[L]];
     LeafRec r;
-    uint32_t nid = 0;
+    uint32_t codes = 0;
     for (int f = 0; f < 4; ++f) {
         const uint32_t nb = tt.neighbors[f];
         r.w[f] = nb == kNone ? kNone : tet2leaf[nb];
-        r.w[4 + f] = tt.verts[f];
-        uint32_t far = kNone;
-        if (nb != kNone) {
-            const tv_tet& o = tets[nb];
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t v = o.verts[j];
-                bool shared = false;
-                for (int k = 0; k < 4; ++k)
-                    if (k != f && tt.verts[k] == v) shared = true;
-                if (!shared) far = v;
-            }
-        }
-        r.w[8 + f] = far;
-        nid |= (static_cast<uint32_t>(tt.normal_ids[f]) & 31u) << (5 * f);
+        // exit_face reads vertex verts[(f+1)&3] of face f (tracer.cpp:152)
+        const uint32_t code = face_code(tt.normal_ids[f]);
+        const uint4 q = verts[tt.verts[(f + 1) & 3]];
+        const uint32_t qq[3] = {q.x, q.y, q.z};
+        r.w[4 + 2 * f] = __float_as_uint(static_cast<float>(qq[code & 3u]) * 0x1.0p-24f);
+        r.w[5 + 2 * f] = __float_as_uint(static_cast<float>(qq[(code >> 2) & 3u]) * 0x1.0p-24f);
+        codes |= code << (8 * f);
     }
-    r.w[12] = nid | (static_cast<uint32_t>(tt.mask) << 20);
+    r.w[12] = codes;
+    mask[L] = tt.mask;
     r.w[13] = __float_as_uint(tt.density);
     r.w[14] = __float_as_uint(tt.temperature);
     r.w[15] = __float_as_uint(tt.albedo);
@@ -235,9 +229,11 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     TRY(dalloc(&g.leaves, g.n_leaves, g.bytes));
     TRY(dalloc(&g.nodes, g.n_internal, g.bytes));
     TRY(dalloc(&g.leaf2tet, g.n_leaves, g.bytes));
+    TRY(dalloc(&g.mask, g.n_leaves, g.bytes));
     CK(cudaMemcpyAsync(g.leaf2tet, order, g.n_leaves * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st), "leaf2tet");
     CK(cudaMemsetAsync(d_depth, 0, sizeof(int), st), "memset");
-    leaves_kernel<<<blocks(g.n_leaves, 256), 256, 0, st>>>(g.tets, order, tet2leaf, g.n_leaves, g.leaves, d_depth);
+    leaves_kernel<<<blocks(g.n_leaves, 256), 256, 0, st>>>(g.tets, order, tet2leaf, g.verts, g.n_leaves, g.leaves,
+                                                            g.mask, d_depth);
     CK(cudaGetLastError(), "leaves_kernel");
     nodes_kernel<<<blocks(nt, 256), 256, 0, st>>>(g.tets, g.verts, nt, tet2leaf, tet2node, g.nodes);
     CK(cudaGetLastError(), "nodes_kernel");
@@ -256,6 +252,7 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     v.nodes = g.nodes;
     v.verts = g.verts;
     v.leaf2tet = g.leaf2tet;
+    v.mask = g.mask;
     for (int r = 0; r < 24; ++r) {
         v.root_ptr[r] = hroot[r];
         v.root_nid[r] = hroot[24 + r];
@@ -275,6 +272,8 @@ void free_grid(DeviceGrid& g) {
     cudaFree(g.leaves);
     cudaFree(g.nodes);
     cudaFree(g.leaf2tet);
+    cudaFree(g.mask);
+    g.mask = nullptr;
     g.tets = nullptr;
     g.verts = nullptr;
     g.leaves = nullptr;

@@ -7,14 +7,27 @@
 
 namespace tvb {
 
-constexpr int kRenderThreads = 128;
-constexpr int kRenderMinBlocks = 4;
+constexpr int kTraceThreads = 128;
+constexpr int kTraceMinBlocks = 4;
+constexpr uint32_t kChunk = 64;               // paths a warp claims per queue atomic
+constexpr uint32_t kInvalidPixel = 0xfffffffeu;
+constexpr uint64_t kMaxBatchPaths = 1ull << 26;
 
-struct TileSched {
-    uint32_t* counter;   // device work counter (zeroed before launch)
-    uint32_t n_units;    // 8 warp units per 16x16 tile of this rank
+// One render batch: this rank's pixels x samples [s0, s0 + ns).
+// Path index p -> unit = p / (ns * 32), s = s0 + (p / 32) % ns, lane = p % 32;
+// a unit is an 8x4 pixel block, 8 units tile a 16x16 sharding tile, and tile
+// t = rank + k * n_ranks (row-major tile numbering).
+struct Batch {
+    uint32_t n_units;
+    uint32_t s0, ns;
     uint32_t tiles_x;
     int32_t rank, n_ranks;
+    uint32_t n_paths;
+    uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
+};
+
+struct StartRec {  // camera ray of one path after TetMarcher::start
+    double dx, dy, dz, t0;
 };
 
 struct RenderOut {
@@ -24,7 +37,10 @@ struct RenderOut {
     uint64_t* stats;  // [cells_visited, paths_traced, degenerate_paths]
 };
 
-__global__ void render_kernel(GridView G, CamView C, RenderParams P, TileSched S, RenderOut O);
+__global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, StartRec* st, uint32_t* cells);
+__global__ void trace_kernel(GridView G, CamView C, RenderParams P, Batch B, const StartRec* st,
+                             const uint32_t* cells, double* rad, uint64_t* stats, uint32_t* counter);
+__global__ void accum_kernel(Batch B, CamView C, const uint32_t* cells, const double* rad, RenderOut O);
 __global__ void march_kernel(GridView G, const tv_ray* rays, uint64_t n, int pass, uint64_t* counts,
                              const uint64_t* offsets, tv_segment* out, uint64_t cap, unsigned long long* deg);
 __global__ void locate_kernel(GridView G, const double* pts, uint64_t n, uint32_t* out);
@@ -42,6 +58,7 @@ struct DeviceGrid {
     LeafRec* leaves = nullptr;
     NodeRec* nodes = nullptr;
     uint32_t* leaf2tet = nullptr;
+    uint8_t* mask = nullptr;
     GridView view{};
     uint64_t bytes = 0;
 };
@@ -54,6 +71,8 @@ void free_grid(DeviceGrid& g);
 // thread-local error plumbing for the C ABI
 int set_error(int code, const std::string& msg);
 int cuda_status(cudaError_t e, const char* what);
+// camera.cpp:12-45 on the host (optional frustum planes for the build)
+int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]);
 
 }  // namespace tvb
 
