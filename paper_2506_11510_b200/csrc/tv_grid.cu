@@ -82,9 +82,9 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
         const uint32_t qq[3] = {q.x, q.y, q.z};
         r.w[4 + 2 * f] = __float_as_uint(static_cast<float>(qq[code & 3u]) * 0x1.0p-24f);
         r.w[5 + 2 * f] = __float_as_uint(static_cast<float>(qq[(code >> 2) & 3u]) * 0x1.0p-24f);
-        codes |= code << (8 * f);
+        codes |= (static_cast<uint32_t>(tt.normal_ids[f]) & 31u) << (5 * f);
     }
-    r.w[12] = codes;
+    r.w[12] = codes | (static_cast<uint32_t>(tt.mask & 7u) << 20);
     mask[L] = tt.mask;
     r.w[13] = __float_as_uint(tt.density);
     r.w[14] = __float_as_uint(tt.temperature);

@@ -11,10 +11,12 @@
 //   start_kernel  camera ray, slab and locate for every path — coherent work,
 //                 kept out of the divergent trace loop;
 //   trace_kernel  persistent warps; each lane traces one path at a time, one
-//                 tet step per loop iteration, and takes a new path from the
-//                 warp's claimed chunk as soon as its path ends (path
-//                 regeneration with warp-level compaction of finished lanes);
-//                 every path's radiance goes to HBM;
+//                 tet step per loop iteration. Path starts and scatter events
+//                 (HG sampling, new flight tables) are deferred and run
+//                 warp-batched, so the rare expensive branches are paid once
+//                 for many lanes; finished lanes take new paths from the warp's
+//                 claimed chunk (path regeneration with warp-level compaction).
+//                 Every path's radiance goes to HBM;
 //   accum_kernel  one thread per pixel adds its samples in order s = 0..spp-1,
 //                 exactly the reference accumulation order
 //                 (path_integrator.hpp:109-114, image.hpp:36-45), so the
@@ -38,6 +40,8 @@ __device__ __forceinline__ void path_pixel(const Batch& B, uint32_t p, int& px, 
     px = static_cast<int>(tx * 16 + (sub & 1u) * 8 + (lane & 7u));
     py = static_cast<int>(ty * 16 + (sub >> 1) * 4 + (lane >> 3));
 }
+
+enum : int { S_IDLE = 0, S_STEP = 1, S_SCATTER = 2 };
 
 }  // namespace
 
@@ -76,7 +80,11 @@ __global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, Sta
 __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
     trace_kernel(GridView G, CamView C, RenderParams P, Batch B, const StartRec* __restrict__ st,
                  const uint32_t* __restrict__ cells, double* __restrict__ rad, uint64_t* stats, uint32_t* counter) {
-    const int lane = threadIdx.x & 31;
+    __shared__ FaceTables<kTraceThreads> S;
+    init_face_tables(S);
+    __syncthreads();
+    const int t = threadIdx.x;
+    const int lane = t & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const d3 cam_pos = mk(C.pos[0], C.pos[1], C.pos[2]);
     const d3 env = mk(P.env[0], P.env[1], P.env[2]);
@@ -85,7 +93,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
     uint32_t chunk_next = 0, chunk_end = 0;  // warp-uniform
     bool exhausted = false;                  // warp-uniform
 
-    bool has = false;
+    int state = S_IDLE;
     uint32_t p = 0, cell = 0, steps = 0;
     int bounce = 0;
     Rng rng;
@@ -96,14 +104,19 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
     LeafRec rec;
 
     for (;;) {
-        // ---- regeneration: idle lanes take consecutive path ids ----
-        const unsigned need = __ballot_sync(kFull, !has);
-        if (need && !(exhausted && chunk_next >= chunk_end)) {
-            const uint32_t n_need = __popc(need);
-            const uint32_t my_rank = __popc(need & lt_mask);
+        const unsigned m_idle = __ballot_sync(kFull, state == S_IDLE);
+        const unsigned m_step = __ballot_sync(kFull, state == S_STEP);
+        const unsigned m_scat = __ballot_sync(kFull, state == S_SCATTER);
+        const bool queue_open = !(exhausted && chunk_next >= chunk_end);
+        if (!m_step && !m_scat && !queue_open) break;
+
+        // ---- regeneration, batched: idle lanes take consecutive path ids ----
+        if (m_idle && queue_open && (__popc(m_idle) >= 8 || !m_step)) {
+            const uint32_t n_need = __popc(m_idle);
+            const uint32_t my_rank = __popc(m_idle & lt_mask);
             uint32_t mine = kNone;
-            uint32_t avail = chunk_end - chunk_next;
-            if (!has && my_rank < avail) mine = chunk_next + my_rank;
+            const uint32_t avail = chunk_end - chunk_next;
+            if (state == S_IDLE && my_rank < avail) mine = chunk_next + my_rank;
             const uint32_t used = min(avail, n_need);
             chunk_next += used;
             if (n_need > avail && !exhausted) {
@@ -117,7 +130,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
                     chunk_end = min(base + kChunk, B.n_paths);
                     const uint32_t avail2 = chunk_end - chunk_next;
                     const uint32_t r2 = my_rank - used;
-                    if (!has && mine == kNone && r2 < avail2) mine = chunk_next + r2;
+                    if (state == S_IDLE && mine == kNone && r2 < avail2) mine = chunk_next + r2;
                     chunk_next += min(avail2, n_need - used);
                 }
             }
@@ -145,15 +158,26 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
                     tau = 0.0;
                     target = -log(1.0 - rng.next());  // path_integrator.hpp:49
                     rec = load_leaf(G.leaves, cell);
-                    has = true;
+                    set_flight_dir(S, t, dir);
+                    state = S_STEP;
                 }
             }
         }
-        if (!__any_sync(kFull, has)) {
-            if (exhausted && chunk_next >= chunk_end) break;
-            continue;
+
+        // ---- scatter, batched: new direction + flight tables (path_integrator.hpp:82, 49) ----
+        if (m_scat && (__popc(m_scat) >= 8 || !m_step)) {
+            if (state == S_SCATTER) {
+                dir = sample_phase_hg(dir, P.g, rng);
+                seg_start = 0.0;
+                probe = 0.0;
+                target = -log(1.0 - rng.next());
+                tau = 0.0;
+                set_flight_dir(S, t, dir);
+                state = S_STEP;
+            }
         }
-        if (!has) continue;
+
+        if (state != S_STEP) continue;
 
         // ---- one tet step: TetMarcher::next (tracer.cpp:47-88) ----
         bool ended = false;
@@ -162,24 +186,28 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
             ++my_deg;
             ended = true;
         } else {
-            double t;
-            int slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+            double tx;
+            d3 pos = ray_at(o, dir, probe);
+            S.pos[0][t] = pos.x, S.pos[1][t] = pos.y, S.pos[2][t] = pos.z;
+            int slot = exit_face_tab(S, t, rec, tx);
             if (slot < 0) {  // degenerate corner: one nudged retry (tracer.cpp:54-61)
                 probe += kNudge;
-                slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+                pos = ray_at(o, dir, probe);
+                S.pos[0][t] = pos.x, S.pos[1][t] = pos.y, S.pos[2][t] = pos.z;
+                slot = exit_face_tab(S, t, rec, tx);
             }
             if (slot < 0) {  // aborted (path_integrator.hpp:62-65)
                 ++my_deg;
                 ended = true;
             } else {
-                const double t_exit = dmax(probe + t, seg_start);
+                const double t_exit = dmax(probe + tx, seg_start);
                 const double lambda = static_cast<double>(__uint_as_float(rec.w[13]));
                 ++my_cells;
                 const double seg_tau = lambda * (t_exit - seg_start);
                 if (lambda > 0.0 && tau + seg_tau >= target) {
-                    // collision: shorten, media, Russian roulette, redirect (path_integrator.hpp:56-82)
+                    // collision: shorten, media, Russian roulette (path_integrator.hpp:56-81)
                     o = ray_at(o, dir, seg_start + (target - tau) / lambda);
-                    const uint32_t mask = G.mask[cell];
+                    const uint32_t mask = rec.w[12] >> 20;
                     if (mask & 2u) {
                         const d3 e = emission_color(static_cast<double>(__uint_as_float(rec.w[14])));
                         L = add(L, mul(mulv(T, e), P.emission_scale));
@@ -197,13 +225,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
                                 else T = divs(T, pmax);
                             }
                         }
-                        if (!ended) {
-                            dir = sample_phase_hg(dir, P.g, rng);
-                            seg_start = 0.0;
-                            probe = 0.0;
-                            target = -log(1.0 - rng.next());
-                            tau = 0.0;
-                        }
+                        if (!ended) state = S_SCATTER;  // redirect is deferred
                     }
                 } else {
                     tau += seg_tau;
@@ -222,7 +244,7 @@ __global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
         }
         if (ended) {
             rad[3ull * p] = result.x, rad[3ull * p + 1] = result.y, rad[3ull * p + 2] = result.z;
-            has = false;
+            state = S_IDLE;
         }
     }
 #pragma unroll
@@ -257,8 +279,8 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
             if (O.counts) n = O.counts[pix];
         }
         for (uint32_t k = 0; k < B.ns; ++k) {
-            const uint64_t p = static_cast<uint64_t>(p0) + k * 32u;
-            const double r = rad[3 * p], g = rad[3 * p + 1], b = rad[3 * p + 2];
+            const uint64_t pp = static_cast<uint64_t>(p0) + k * 32u;
+            const double r = rad[3 * pp], g = rad[3 * pp + 1], b = rad[3 * pp + 2];
             sr += r, sg += g, sb += b;
             qr += r * r, qg += g * g, qb += b * b;
             ++n;
