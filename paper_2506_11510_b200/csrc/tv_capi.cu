@@ -159,7 +159,7 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
         int per_sm = 1;
         cudaFuncSetAttribute(trace_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             cudaSharedmemCarveoutMaxShared);
+                             60);
         cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel, kTraceThreads, 0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);

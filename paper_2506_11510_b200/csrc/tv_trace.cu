@@ -77,186 +77,7 @@ __global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, Sta
     }
 }
 
-__global__ void __launch_bounds__(kTraceThreads, kTraceMinBlocks)
-    trace_kernel(GridView G, CamView C, RenderParams P, Batch B, const StartRec* __restrict__ st,
-                 const uint32_t* __restrict__ cells, double* __restrict__ rad, uint64_t* stats, uint32_t* counter) {
-    __shared__ FaceTables<kTraceThreads> S;
-    init_face_tables(S);
-    __syncthreads();
-    const int t = threadIdx.x;
-    const int lane = t & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    const d3 cam_pos = mk(C.pos[0], C.pos[1], C.pos[2]);
-    const d3 env = mk(P.env[0], P.env[1], P.env[2]);
-    uint64_t my_cells = 0, my_deg = 0;
-
-    uint32_t chunk_next = 0, chunk_end = 0;  // warp-uniform
-    bool exhausted = false;                  // warp-uniform
-
-    int state = S_IDLE;
-    uint32_t p = 0, cell = 0, steps = 0;
-    int bounce = 0;
-    Rng rng;
-    rng.key = 0;
-    rng.dim = 0;
-    d3 o = cam_pos, dir = mk(0, 0, 1), T = mk(1, 1, 1), L = mk(0, 0, 0);
-    double seg_start = 0.0, probe = 0.0, tau = 0.0, target = 0.0;
-    LeafRec rec;
-
-    for (;;) {
-        const unsigned m_idle = __ballot_sync(kFull, state == S_IDLE);
-        const unsigned m_step = __ballot_sync(kFull, state == S_STEP);
-        const unsigned m_scat = __ballot_sync(kFull, state == S_SCATTER);
-        const bool queue_open = !(exhausted && chunk_next >= chunk_end);
-        if (!m_step && !m_scat && !queue_open) break;
-
-        // ---- regeneration, batched: idle lanes take consecutive path ids ----
-        if (m_idle && queue_open && (__popc(m_idle) >= 8 || !m_step)) {
-            const uint32_t n_need = __popc(m_idle);
-            const uint32_t my_rank = __popc(m_idle & lt_mask);
-            uint32_t mine = kNone;
-            const uint32_t avail = chunk_end - chunk_next;
-            if (state == S_IDLE && my_rank < avail) mine = chunk_next + my_rank;
-            const uint32_t used = min(avail, n_need);
-            chunk_next += used;
-            if (n_need > avail && !exhausted) {
-                uint32_t base = 0;
-                if (lane == 0) base = atomicAdd(counter, kChunk);
-                base = __shfl_sync(kFull, base, 0);
-                if (base >= B.n_paths) {
-                    exhausted = true;
-                } else {
-                    chunk_next = base;
-                    chunk_end = min(base + kChunk, B.n_paths);
-                    const uint32_t avail2 = chunk_end - chunk_next;
-                    const uint32_t r2 = my_rank - used;
-                    if (state == S_IDLE && mine == kNone && r2 < avail2) mine = chunk_next + r2;
-                    chunk_next += min(avail2, n_need - used);
-                }
-            }
-            if (mine != kNone) {
-                const uint32_t c = cells[mine];
-                if (c == kNone) {  // ray misses the grid: trace_path returns env (path_integrator.hpp:46)
-                    rad[3ull * mine] = env.x, rad[3ull * mine + 1] = env.y, rad[3ull * mine + 2] = env.z;
-                } else if (c != kInvalidPixel) {
-                    int px, py;
-                    uint32_t s;
-                    path_pixel(B, mine, px, py, s);
-                    const StartRec sr = st[mine];
-                    rng.init(P.seed, static_cast<uint64_t>(py) * static_cast<uint64_t>(C.w) + px, s);
-                    rng.dim = 2;  // the jitter draws
-                    p = mine;
-                    cell = c;
-                    o = cam_pos;
-                    dir = mk(sr.dx, sr.dy, sr.dz);
-                    seg_start = sr.t0;
-                    probe = sr.t0 + kNudge;
-                    T = mk(1, 1, 1);
-                    L = mk(0, 0, 0);
-                    bounce = 0;
-                    steps = 0;
-                    tau = 0.0;
-                    target = -log(1.0 - rng.next());  // path_integrator.hpp:49
-                    rec = load_leaf(G.leaves, cell);
-                    set_flight_dir(S, t, dir);
-                    state = S_STEP;
-                }
-            }
-        }
-
-        // ---- scatter, batched: new direction + flight tables (path_integrator.hpp:82, 49) ----
-        if (m_scat && (__popc(m_scat) >= 8 || !m_step)) {
-            if (state == S_SCATTER) {
-                dir = sample_phase_hg(dir, P.g, rng);
-                seg_start = 0.0;
-                probe = 0.0;
-                target = -log(1.0 - rng.next());
-                tau = 0.0;
-                set_flight_dir(S, t, dir);
-                state = S_STEP;
-            }
-        }
-
-        if (state != S_STEP) continue;
-
-        // ---- one tet step: TetMarcher::next (tracer.cpp:47-88) ----
-        bool ended = false;
-        d3 result = L;
-        if (++steps > kMaxSteps) {
-            ++my_deg;
-            ended = true;
-        } else {
-            double tx;
-            d3 pos = ray_at(o, dir, probe);
-            S.pos[0][t] = pos.x, S.pos[1][t] = pos.y, S.pos[2][t] = pos.z;
-            int slot = exit_face_tab(S, t, rec, tx);
-            if (slot < 0) {  // degenerate corner: one nudged retry (tracer.cpp:54-61)
-                probe += kNudge;
-                pos = ray_at(o, dir, probe);
-                S.pos[0][t] = pos.x, S.pos[1][t] = pos.y, S.pos[2][t] = pos.z;
-                slot = exit_face_tab(S, t, rec, tx);
-            }
-            if (slot < 0) {  // aborted (path_integrator.hpp:62-65)
-                ++my_deg;
-                ended = true;
-            } else {
-                const double t_exit = dmax(probe + tx, seg_start);
-                const double lambda = static_cast<double>(__uint_as_float(rec.w[13]));
-                ++my_cells;
-                const double seg_tau = lambda * (t_exit - seg_start);
-                if (lambda > 0.0 && tau + seg_tau >= target) {
-                    // collision: shorten, media, Russian roulette (path_integrator.hpp:56-81)
-                    o = ray_at(o, dir, seg_start + (target - tau) / lambda);
-                    const uint32_t mask = rec.w[12] >> 20;
-                    if (mask & 2u) {
-                        const d3 e = emission_color(static_cast<double>(__uint_as_float(rec.w[14])));
-                        L = add(L, mul(mulv(T, e), P.emission_scale));
-                    }
-                    T = mul(T, (mask & 4u) ? static_cast<double>(__uint_as_float(rec.w[15])) : P.default_albedo);
-                    ++bounce;
-                    result = L;
-                    if (bounce >= P.max_bounces) {
-                        ended = true;
-                    } else {
-                        if (bounce >= 4) {
-                            const double pmax = dmax(T.x, dmax(T.y, T.z));
-                            if (pmax < 1e-3) {
-                                if (rng.next() >= pmax) ended = true;
-                                else T = divs(T, pmax);
-                            }
-                        }
-                        if (!ended) state = S_SCATTER;  // redirect is deferred
-                    }
-                } else {
-                    tau += seg_tau;
-                    const uint32_t nb = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot);
-                    if (nb == kNone) {  // escaped (path_integrator.hpp:66)
-                        result = add(L, mulv(T, env));
-                        ended = true;
-                    } else {
-                        cell = nb;
-                        rec = load_leaf(G.leaves, nb);
-                        seg_start = t_exit;
-                        probe = t_exit + kNudge;
-                    }
-                }
-            }
-        }
-        if (ended) {
-            rad[3ull * p] = result.x, rad[3ull * p + 1] = result.y, rad[3ull * p + 2] = result.z;
-            state = S_IDLE;
-        }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        my_cells += __shfl_down_sync(kFull, my_cells, off);
-        my_deg += __shfl_down_sync(kFull, my_deg, off);
-    }
-    if (lane == 0 && stats) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(stats), static_cast<unsigned long long>(my_cells));
-        atomicAdd(reinterpret_cast<unsigned long long*>(stats + 2), static_cast<unsigned long long>(my_deg));
-    }
-}
+#include "tv_path.inc"
 
 // ImageAccumulator::add_sample in sample order (image.hpp:36-45); one thread
 // per pixel of the batch's units.

@@ -8,7 +8,7 @@
 namespace tvb {
 
 constexpr int kTraceThreads = 128;
-constexpr int kTraceMinBlocks = 4;
+constexpr int kTraceMinBlocks = 5;
 constexpr uint32_t kChunk = 64;               // paths a warp claims per queue atomic
 constexpr uint32_t kInvalidPixel = 0xfffffffeu;
 constexpr uint64_t kMaxBatchPaths = 1ull << 26;
