@@ -136,8 +136,15 @@ struct Workspace {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int trace_blocks = 0, sms = 0;
+    TraceFn trace = nullptr;
+    uint32_t regen_min = 8, scatter_min = 8;
 };
 Workspace g_ws[64];
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
 
 int grow(void*& p, size_t& have, size_t need) {
     if (have >= need) return TV_OK;
@@ -157,11 +164,17 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaEventCreate(&w.ev0), "event create");
         TV_CK(cudaEventCreate(&w.ev1), "event create");
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
+        // tuning knobs (defaults are the measured best on B200)
+        const int minb = env_int("TV_TRACE_MINB", 5);
+        w.trace = trace_variant(minb);
+        w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 8));
+        w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 8));
         int per_sm = 1;
-        cudaFuncSetAttribute(trace_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             60);
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
+                             env_int("TV_CARVEOUT", 60));
         cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trace_kernel, kTraceThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace), kTraceThreads,
+                                                      0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
     }
     out = &w;
@@ -199,12 +212,14 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.n_ranks = n_ranks;
         B.n_paths = static_cast<uint32_t>(units * 32 * B.ns);
         B.first = s0 == 0 ? 1u : 0u;
+        B.regen_min = w.regen_min;
+        B.scatter_min = w.scatter_min;
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
         start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);
         TV_CK(cudaGetLastError(), "start_kernel launch");
         TV_CK(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), st), "memset counter");
-        trace_kernel<<<w.trace_blocks, kTraceThreads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
-                                                               w.counter);
+        w.trace<<<w.trace_blocks, kTraceThreads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
+                                                          w.counter);
         TV_CK(cudaGetLastError(), "trace_kernel launch");
         const unsigned ab = static_cast<unsigned>(std::min<uint64_t>((units * 32 + 127) / 128, w.sms * 16ull));
         accum_kernel<<<ab, 128, 0, st>>>(B, cv, cells, rad, out);

@@ -24,6 +24,7 @@ struct Batch {
     int32_t rank, n_ranks;
     uint32_t n_paths;
     uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
+    uint32_t regen_min, scatter_min;  // warp-batching thresholds of the trace loop
 };
 
 struct StartRec {  // camera ray of one path after TetMarcher::start
@@ -38,8 +39,10 @@ struct RenderOut {
 };
 
 __global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, StartRec* st, uint32_t* cells);
-__global__ void trace_kernel(GridView G, CamView C, RenderParams P, Batch B, const StartRec* st,
-                             const uint32_t* cells, double* rad, uint64_t* stats, uint32_t* counter);
+using TraceFn = void (*)(GridView, CamView, RenderParams, Batch, const StartRec*, const uint32_t*, double*,
+                         uint64_t*, uint32_t*);
+// trace kernel instantiated for 4, 5, 6 or 8 resident blocks per SM
+TraceFn trace_variant(int min_blocks);
 __global__ void accum_kernel(Batch B, CamView C, const uint32_t* cells, const double* rad, RenderOut O);
 __global__ void march_kernel(GridView G, const tv_ray* rays, uint64_t n, int pass, uint64_t* counts,
                              const uint64_t* offsets, tv_segment* out, uint64_t cap, unsigned long long* deg);
