@@ -165,13 +165,13 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaEventCreate(&w.ev1), "event create");
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
         // tuning knobs (defaults are the measured best on B200)
-        const int minb = env_int("TV_TRACE_MINB", 5);
+        const int minb = env_int("TV_TRACE_MINB", 4);
         w.trace = trace_variant(minb);
-        w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 8));
-        w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 8));
+        w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
+        w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 1));
         int per_sm = 1;
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
-                             env_int("TV_CARVEOUT", 60));
+                             env_int("TV_CARVEOUT", 50));
         cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace), kTraceThreads,
                                                       0);
