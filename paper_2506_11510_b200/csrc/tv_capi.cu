@@ -137,7 +137,7 @@ struct Workspace {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int trace_blocks = 0, sms = 0;
     TraceFn trace = nullptr;
-    uint32_t regen_min = 8, scatter_min = 8;
+    uint32_t regen_min = 8, scatter_min = 8, prefetch = 0, order = 0;
 };
 Workspace g_ws[64];
 
@@ -169,6 +169,8 @@ int workspace(int device, Workspace*& out) {
         w.trace = trace_variant(minb);
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 1));
+        w.prefetch = static_cast<uint32_t>(env_int("TV_PREFETCH", 0));
+        w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
         int per_sm = 1;
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
                              env_int("TV_CARVEOUT", 50));
@@ -214,6 +216,8 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.first = s0 == 0 ? 1u : 0u;
         B.regen_min = w.regen_min;
         B.scatter_min = w.scatter_min;
+        B.prefetch = w.prefetch;
+        B.order = w.order;
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
         start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);
         TV_CK(cudaGetLastError(), "start_kernel launch");

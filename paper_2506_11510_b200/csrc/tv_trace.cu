@@ -29,11 +29,24 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Path id of (unit, pixel lane, sample k of the batch). order 0: the 32
+// pixels of a unit for one sample are consecutive; order 1: the samples of one
+// pixel are consecutive, so a warp traces many samples of few pixels.
+__device__ __forceinline__ uint32_t path_id(const Batch& B, uint32_t unit, uint32_t lane, uint32_t k) {
+    return unit * B.ns * 32u + (B.order ? lane * B.ns + k : k * 32u + lane);
+}
+
 __device__ __forceinline__ void path_pixel(const Batch& B, uint32_t p, int& px, int& py, uint32_t& s) {
     const uint32_t per_unit = B.ns * 32u;
     const uint32_t unit = p / per_unit, r = p - unit * per_unit;
-    s = B.s0 + r / 32u;
-    const uint32_t lane = r & 31u;
+    uint32_t lane;
+    if (B.order) {
+        lane = r / B.ns;
+        s = B.s0 + (r - lane * B.ns);
+    } else {
+        s = B.s0 + r / 32u;
+        lane = r & 31u;
+    }
     const uint32_t k = unit >> 3, sub = unit & 7u;
     const uint32_t t = static_cast<uint32_t>(B.rank) + k * static_cast<uint32_t>(B.n_ranks);
     const uint32_t tx = t % B.tiles_x, ty = t / B.tiles_x;
@@ -86,7 +99,7 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
     const uint32_t n_px = B.n_units * 32u;
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_px; q += gridDim.x * blockDim.x) {
         const uint32_t unit = q >> 5, lane = q & 31u;
-        const uint32_t p0 = unit * B.ns * 32u + lane;
+        const uint32_t p0 = path_id(B, unit, lane, 0);
         int px, py;
         uint32_t s;
         path_pixel(B, p0, px, py, s);
@@ -100,7 +113,7 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
             if (O.counts) n = O.counts[pix];
         }
         for (uint32_t k = 0; k < B.ns; ++k) {
-            const uint64_t pp = static_cast<uint64_t>(p0) + k * 32u;
+            const uint64_t pp = path_id(B, unit, lane, k);
             const double r = rad[3 * pp], g = rad[3 * pp + 1], b = rad[3 * pp + 2];
             sr += r, sg += g, sb += b;
             qr += r * r, qg += g * g, qb += b * b;

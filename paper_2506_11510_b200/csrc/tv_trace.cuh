@@ -25,6 +25,8 @@ struct Batch {
     uint32_t n_paths;
     uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
     uint32_t regen_min, scatter_min;  // warp-batching thresholds of the trace loop
+    uint32_t prefetch;                // 0 none, 1 neighbour records to L1, 2 to L2
+    uint32_t order;                   // path id order (see path_id in tv_trace.cu)
 };
 
 struct StartRec {  // camera ray of one path after TetMarcher::start
