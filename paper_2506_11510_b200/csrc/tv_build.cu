@@ -1286,6 +1286,24 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
 
 using namespace tvb;
 
+namespace {
+// The reference validates BuildConfig and constructs the camera before any
+// work (builder.cpp:120-121, camera.cpp:15-20); so do we, before touching the
+// device.
+int prevalidate(const tv_build_config* cfg, const tv_camera* camera) {
+    int rc = validate_build_cfg(cfg);
+    if (rc) return rc;
+    if (cfg->use_camera && !camera) return set_error(TV_ERR_CONFIG, "useCamera set but no camera given");
+    if (camera) {
+        CamView cv;
+        d3 pn[5];
+        double pd[5];
+        if ((rc = host_camera(camera, cv, pn, pd))) return rc;
+    }
+    return TV_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, double value, float* out_dev,
@@ -1307,6 +1325,8 @@ int tv_build_dev(const float* density_dev, const float* temperature_dev, const f
                  tv_grid** out, tv_build_stats* stats) {
     if (!out || !density_dev) return set_error(TV_ERR_ARG, "null argument");
     *out = nullptr;
+    int rc = prevalidate(cfg, camera);
+    if (rc) return rc;
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return set_error(TV_ERR_CUDA, "no CUDA device available");
     cudaError_t e = cudaSetDevice(device);
@@ -1320,6 +1340,8 @@ int tv_build(const float* density, const float* temperature, const float* albedo
     if (!out || !density) return set_error(TV_ERR_ARG, "null argument");
     *out = nullptr;
     if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR_CONFIG, "volume dimensions must be positive");
+    int rc0 = prevalidate(cfg, camera);
+    if (rc0) return rc0;
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return set_error(TV_ERR_CUDA, "no CUDA device available");
     cudaError_t e = cudaSetDevice(device);
