@@ -72,13 +72,18 @@ typedef struct {
 } tv_tet;
 
 /* PinholeCamera constructor arguments (camera.hpp:18-19). The basis, tan and
- * frustum planes are derived on the host exactly as camera.cpp:12-45 does. */
+ * frustum planes are derived on the host exactly as camera.cpp:12-45 does.
+ * basis_final != 0 means forward/up are an already constructed camera's
+ * forward() / up() (unit, orthogonal; camera.hpp:37-39): they are used as-is,
+ * so a reference PinholeCamera converts without re-normalising (bit-exact). */
 typedef struct {
     double position[3];
     double forward[3];
     double up[3];
     double vfov_degrees;
     int32_t width, height;
+    int32_t basis_final;
+    int32_t pad;
 } tv_camera;
 
 /* RenderConfig (tracer.hpp:16-28). exposure/gamma only affect 8-bit output. */

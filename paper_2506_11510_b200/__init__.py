@@ -69,7 +69,8 @@ def _check(rc: int):
 # ------------------------------------------------------------- C structs ---
 class _Camera(C.Structure):
     _fields_ = [("position", C.c_double * 3), ("forward", C.c_double * 3), ("up", C.c_double * 3),
-                ("vfov_degrees", C.c_double), ("width", C.c_int32), ("height", C.c_int32)]
+                ("vfov_degrees", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
+                ("basis_final", C.c_int32), ("pad", C.c_int32)]
 
 
 class _RenderConfig(C.Structure):

@@ -1362,9 +1362,4 @@ int tv_build(const float* density, const float* temperature, const float* albedo
     return rc;
 }
 
-int tv_render_regular(const float*, int32_t, int32_t, int32_t, double, const tv_camera*, const tv_render_config*, int,
-                      tv_framebuffer*, tv_render_stats*) {
-    return set_error(TV_ERR, "tv_render_regular: not available in this build");
-}
-
 }  // extern "C"

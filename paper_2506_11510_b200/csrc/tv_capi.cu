@@ -49,10 +49,14 @@ int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]) {
     const d3 f = mk(c->forward[0], c->forward[1], c->forward[2]);
     const d3 up = mk(c->up[0], c->up[1], c->up[2]);
     if (std::sqrt(dot(f, f)) == 0.0) return set_error(TV_ERR_CAMERA, "forward vector must be nonzero");
-    const d3 fwd = normalize(f);
-    const d3 upo = sub(up, mul(fwd, dot(up, fwd)));
-    if (std::sqrt(dot(upo, upo)) < 1e-12) return set_error(TV_ERR_CAMERA, "up vector is parallel to the view direction");
-    const d3 upn = normalize(upo);
+    d3 fwd = f, upn = up;
+    if (!c->basis_final) {
+        fwd = normalize(f);
+        const d3 upo = sub(up, mul(fwd, dot(up, fwd)));
+        if (std::sqrt(dot(upo, upo)) < 1e-12)
+            return set_error(TV_ERR_CAMERA, "up vector is parallel to the view direction");
+        upn = normalize(upo);
+    }
     const d3 right = cross(upn, fwd);
     const double kPi = 3.14159265358979323846;
     v.pos[0] = c->position[0], v.pos[1] = c->position[1], v.pos[2] = c->position[2];
@@ -100,6 +104,12 @@ int validate_render(const tv_render_config* r) {
     if (!(r->gamma > 0.0)) return set_error(TV_ERR_CONFIG, "gamma must be positive");
     return TV_OK;
 }
+
+}  // namespace
+
+int validate_render_cfg(const tv_render_config* r) { return validate_render(r); }
+
+namespace {
 
 RenderParams make_params(const tv_render_config* r) {
     RenderParams p;

@@ -1,0 +1,114 @@
+// Drop-in check of include/tetvol_b200.hpp against the UNMODIFIED reference
+// library (linked from oracle/_ref): the same TetGrid / PinholeCamera /
+// RenderConfig / BuildConfig values go through tetvol:: (CPU) and
+// tetvol::b200:: (GPU), and the results must be bit-identical.
+// Built by tests/cpp/Makefile; run by tests/test_gpu_shim.py on a GPU box.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "tetvol_b200.hpp"
+
+using namespace tetvol;
+
+static DenseVolume blob(int n) {
+    DenseVolume v(n, n, n);
+    auto& d = v.channel("density");
+    for (int k = 0; k < n; ++k)
+        for (int j = 0; j < n; ++j)
+            for (int i = 0; i < n; ++i) {
+                Vec3 p = v.voxel_center(i, j, k) - Vec3{0.5, 0.5, 0.5};
+                double t = std::max(0.0, 1.0 - length_sq(p) / (0.45 * 0.45));
+                d[v.index(i, j, k)] = static_cast<float>(t * t);
+            }
+    return v;
+}
+
+static std::vector<std::array<uint32_t, 12>> leaf_set(const TetGrid& g) {
+    std::vector<std::array<uint32_t, 12>> out;
+    for (TetId t : g.leaf_ids()) {
+        std::array<std::array<uint32_t, 3>, 4> c;
+        for (int k = 0; k < 4; ++k) c[k] = g.vertex(g.tet(t).verts[k]).q;
+        std::sort(c.begin(), c.end());
+        std::array<uint32_t, 12> key;
+        for (int k = 0; k < 4; ++k)
+            for (int a = 0; a < 3; ++a) key[3 * k + a] = c[k][a];
+        out.push_back(key);
+    }
+    std::sort(out.begin(), out.end());
+    return out;
+}
+
+#define REQUIRE(x)                                                       \
+    do {                                                                 \
+        if (!(x)) {                                                      \
+            std::fprintf(stderr, "FAILED %s:%d: %s\n", __FILE__, __LINE__, #x); \
+            return 1;                                                    \
+        }                                                                \
+    } while (0)
+
+int main() {
+    DenseVolume vol = blob(48);
+    BuildConfig bc;
+    bc.variation_threshold = 0.15;
+    bc.max_level = 11;
+    bc.density_scale = 8.0;
+    TetGrid ref = build_adaptive_grid(vol, bc);
+    PinholeCamera cam({0.5, 0.5, -2}, {0, 0.05, 1}, {0, 1, 0}, 40, 96, 80);
+    RenderConfig rc;
+    rc.spp = 4;
+    rc.max_bounces = 16;
+    rc.seed = 5;
+    rc.hg_g = 0.2;
+
+    // render(): reference CPU vs GPU on the same uploaded grid
+    ImageAccumulator a = render(ref, cam, rc, 0);
+    b200::DeviceGrid dg(ref);
+    ImageAccumulator b = b200::render(dg, cam, rc);
+    REQUIRE(a.cells_visited == b.cells_visited);
+    REQUIRE(a.degenerate_paths == b.degenerate_paths);
+    REQUIRE(std::memcmp(a.sum.data(), b.sum.data(), a.sum.size() * sizeof(double)) == 0);
+    REQUIRE(std::memcmp(a.sum_sq.data(), b.sum_sq.data(), a.sum_sq.size() * sizeof(double)) == 0);
+    REQUIRE(a.sample_counts == b.sample_counts);
+
+    // build_adaptive_grid(): GPU build, downloaded, passes validate(), same leaves
+    BuildStats st;
+    b200::DeviceGrid built = b200::build_adaptive_grid(vol, bc, nullptr, &st);
+    TetGrid back = built.download();
+    REQUIRE(back.validate().ok);
+    REQUIRE(back.leaf_count() == ref.leaf_count());
+    REQUIRE(leaf_set(back) == leaf_set(ref));
+
+    // march_segments(): batched on the GPU vs per ray on the CPU
+    std::vector<Ray> rays;
+    for (int i = 0; i < 500; ++i) {
+        RngStream r(3, 7, i);
+        Vec3 o{r.next() * 3 - 1, r.next() * 3 - 1, -1.5};
+        Vec3 t{0.2 + 0.6 * r.next(), 0.2 + 0.6 * r.next(), 0.2 + 0.6 * r.next()};
+        rays.push_back(Ray{o, normalize(t - o)});
+    }
+    auto segs = b200::march_segments(dg, rays);
+    for (size_t i = 0; i < rays.size(); ++i) {
+        auto want = march_segments(ref, rays[i]);
+        REQUIRE(want.size() == segs[i].size());
+        for (size_t k = 0; k < want.size(); ++k) {
+            REQUIRE(want[k].cell == segs[i][k].cell);
+            REQUIRE(want[k].t_enter == segs[i][k].t_enter);
+            REQUIRE(want[k].t_exit == segs[i][k].t_exit);
+        }
+    }
+
+    // exceptions map back to the reference types
+    try {
+        RenderConfig bad;
+        bad.spp = 0;
+        b200::render(dg, cam, bad);
+        REQUIRE(false);
+    } catch (const ConfigError&) {
+    }
+    std::printf("shim ok: %zu leaves, %llu cells, framebuffer bit-identical\n", ref.leaf_count(),
+                static_cast<unsigned long long>(b.cells_visited));
+    return 0;
+}
