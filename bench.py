@@ -62,7 +62,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -216,7 +216,6 @@ def main():
     words = tv.tile_pack_words(W_IMG, H_IMG, rank, world, 3)
     packed = torch.zeros(words, dtype=torch.float64, device="cuda")
     gathered = torch.zeros(words * world, dtype=torch.float64, device="cuda")
-    launches_per_step = 1 + (2 + world if world > 1 else 0)
     k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
@@ -253,6 +252,10 @@ def main():
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
     kern_ms = float(np.mean([k_start[i].elapsed_time(k_end[i]) for i in range(args.steps)]))
+    # per-kernel device time of the last timed frame (CUDA events recorded by the
+    # library on `stream` around start / trace / accumulate)
+    timing = tv.last_frame_timing(dev)
+    trace_ms = timing["trace_ms"]
     st = stats.cpu().numpy()
     cells_rank = int(st[0]) // args.steps
     if world > 1:
@@ -306,9 +309,9 @@ def main():
 
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
-    achieved = cells_rank * BYTES_PER_STEP / (kern_ms * 1e-3) / 1e9
+    achieved = cells_rank * BYTES_PER_STEP / (trace_ms * 1e-3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "render_kernel_dram.json")
+    prof = os.path.join(ROOT, "profiles", "trace_kernel_dram.json")
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
@@ -316,8 +319,10 @@ def main():
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": "render_kernel", "kernel_ms": kern_ms,
+                "traffic": traffic, "kernel": "trace_kernel", "kernel_ms": trace_ms,
+                "frame_kernels_ms": {"start": timing["start_ms"], "trace": trace_ms, "accumulate": timing["accum_ms"]},
                 "bytes_per_step": BYTES_PER_STEP, "tet_steps_per_launch": cells_rank,
+                "algorithmic_bytes_per_launch": cells_rank * BYTES_PER_STEP,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s"}
 
     cpu = None
@@ -343,7 +348,8 @@ def main():
                        "build_s_device": bst.seconds},
             "tet_steps_per_s": cells_frame / (ms * 1e-3), "cells_per_path": cells_frame / samples,
             "ms_per_frame": ms, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+            "gpu_launches": (timing["launches"] + (1 + world if world > 1 else 0)) * args.steps,
+            "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -204,6 +204,10 @@ int tv_render(const tv_grid* g, const tv_camera* camera, const tv_render_config*
 int tv_render_tiles(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg, int32_t rank,
                     int32_t n_ranks, double* sum_dev, double* sum_sq_dev, uint32_t* counts_dev, uint64_t* stats_dev,
                     void* stream);
+/* Device time (ms) of the last frame rendered on `device`, per kernel:
+ * out[0] start (camera rays + locate), out[1] trace, out[2] accumulate;
+ * out[3] = number of kernel launches of that frame. Synchronises on it. */
+int tv_last_frame_timing(int device, double out[4]);
 /* Packs this rank's tiles of a full-frame device buffer (elem_words 64-bit
  * words per pixel) into a contiguous buffer of tv_tile_pack_words() words
  * (for one NCCL all-gather), and the inverse for the gathered buffers. */

@@ -137,6 +137,7 @@ _sig("tv_render", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.P
 _sig("tv_render_tiles", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.c_int32, C.c_int32, _P, _P, _P,
      _P, _P)
 _sig("tv_tile_pack_words", C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32)
+_sig("tv_last_frame_timing", C.c_int, C.c_int, C.POINTER(C.c_double))
 _sig("tv_tile_pack", C.c_int, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P)
 _sig("tv_tile_unpack", C.c_int, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P)
 _sig("tv_march_segments", C.c_int, _P, _P, C.c_uint64, _P, _U64, C.c_uint64, _U64, _U64)
@@ -362,6 +363,13 @@ def render_tiles(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, rank: 
     cam, rc = camera._c(), cfg._c()
     _check(_lib.tv_render_tiles(grid.handle, C.byref(cam), C.byref(rc), int(rank), int(n_ranks), sum_dev, sum_sq_dev,
                                 counts_dev, stats_dev, stream))
+
+
+def last_frame_timing(device: int = 0) -> dict:
+    """Device ms of the last frame's kernels (start, trace, accumulate) and its launch count."""
+    out = (C.c_double * 4)()
+    _check(_lib.tv_last_frame_timing(int(device), out))
+    return dict(start_ms=out[0], trace_ms=out[1], accum_ms=out[2], launches=int(out[3]))
 
 
 def tile_pack_words(width: int, height: int, rank: int, n_ranks: int, elem_words: int) -> int:

@@ -148,7 +148,10 @@ struct Workspace {
     int trace_blocks = 0, sms = 0;
     TraceFn trace = nullptr;
     uint32_t regen_min = 8, scatter_min = 8, prefetch = 0, order = 0;
+    cudaEvent_t tev[4 * 8] = {};  // per-batch kernel boundaries of the last frame
+    int n_timed = 0, n_launches = 0;
 };
+constexpr int kTimedBatches = 8;
 Workspace g_ws[64];
 
 int env_int(const char* name, int dflt) {
@@ -214,7 +217,15 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
     StartRec* st_rec = reinterpret_cast<StartRec*>(base);
     double* rad = reinterpret_cast<double*>(base + max_paths * sizeof(StartRec));
     uint32_t* cells = reinterpret_cast<uint32_t*>(base + max_paths * (sizeof(StartRec) + 3 * sizeof(double)));
+    if (!w.tev[0]) {
+        for (auto& e : w.tev) TV_CK(cudaEventCreate(&e), "event create");
+    }
+    w.n_timed = 0;
+    w.n_launches = 0;
     for (uint64_t s0 = 0; s0 < static_cast<uint64_t>(rp.spp); s0 += ns) {
+        cudaEvent_t* ev = w.n_timed < kTimedBatches ? &w.tev[4 * w.n_timed] : nullptr;
+        if (ev) ++w.n_timed;
+        w.n_launches += 3;
         Batch B;
         B.n_units = static_cast<uint32_t>(units);
         B.s0 = static_cast<uint32_t>(s0);
@@ -229,15 +240,39 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.prefetch = w.prefetch;
         B.order = w.order;
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
+        if (ev) TV_CK(cudaEventRecord(ev[0], st), "event");
         start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);
         TV_CK(cudaGetLastError(), "start_kernel launch");
         TV_CK(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), st), "memset counter");
+        if (ev) TV_CK(cudaEventRecord(ev[1], st), "event");
         w.trace<<<w.trace_blocks, kTraceThreads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
                                                           w.counter);
         TV_CK(cudaGetLastError(), "trace_kernel launch");
+        if (ev) TV_CK(cudaEventRecord(ev[2], st), "event");
         const unsigned ab = static_cast<unsigned>(std::min<uint64_t>((units * 32 + 127) / 128, w.sms * 16ull));
         accum_kernel<<<ab, 128, 0, st>>>(B, cv, cells, rad, out);
         TV_CK(cudaGetLastError(), "accum_kernel launch");
+        if (ev) TV_CK(cudaEventRecord(ev[3], st), "event");
+    }
+    return TV_OK;
+}
+
+// Device time of the last frame's kernels on this device (sums over batches):
+// out[0] start, out[1] trace, out[2] accumulate (ms); out[3] kernel launches.
+int last_frame_timing(int device, double* out) {
+    Workspace* w;
+    int rc = workspace(device, w);
+    if (rc) return rc;
+    out[0] = out[1] = out[2] = 0.0;
+    out[3] = w->n_launches;
+    for (int b = 0; b < w->n_timed; ++b) {
+        cudaEvent_t* ev = &w->tev[4 * b];
+        TV_CK(cudaEventSynchronize(ev[3]), "timing sync");
+        for (int k = 0; k < 3; ++k) {
+            float ms = 0.f;
+            TV_CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]), "elapsed");
+            out[k] += ms;
+        }
     }
     return TV_OK;
 }
@@ -426,6 +461,13 @@ int tv_render_tiles(const tv_grid* h, const tv_camera* camera, const tv_render_c
     std::lock_guard<std::mutex> lk(w->mu);
     RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
     return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream));
+}
+
+int tv_last_frame_timing(int device, double out[4]) {
+    if (!out) return set_error(TV_ERR_ARG, "out is null");
+    int rc = use_device(device);
+    if (rc) return rc;
+    return last_frame_timing(device, out);
 }
 
 int tv_march_segments(const tv_grid* h, const tv_ray* rays, uint64_t n, tv_segment* out, uint64_t* offsets,
