@@ -229,6 +229,10 @@ int tv_locate_points(const tv_grid* g, const double* points, uint64_t n, uint32_
 int tv_render_regular(const float* density, int32_t nx, int32_t ny, int32_t nz, double density_scale,
                       const tv_camera* camera, const tv_render_config* cfg, int device, tv_framebuffer* out,
                       tv_render_stats* stats);
+/* Same, with the density already in HBM (f32, x fastest). */
+int tv_render_regular_dev(const float* density_dev, int32_t nx, int32_t ny, int32_t nz, double density_scale,
+                          const tv_camera* camera, const tv_render_config* cfg, int device, tv_framebuffer* out,
+                          tv_render_stats* stats);
 
 #ifdef __cplusplus
 }

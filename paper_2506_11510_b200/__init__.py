@@ -144,6 +144,8 @@ _sig("tv_march_segments", C.c_int, _P, _P, C.c_uint64, _P, _U64, C.c_uint64, _U6
 _sig("tv_locate_points", C.c_int, _P, _D, C.c_uint64, _U32)
 _sig("tv_render_regular", C.c_int, _F, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
      C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
+_sig("tv_render_regular_dev", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
+     C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
 
 # reference Tet layout (tet_grid.hpp:64-75; 68 bytes)
 TET_DTYPE = np.dtype([("verts", "<u4", 4), ("children", "<u4", 2), ("parent", "<u4"), ("neighbors", "<u4", 4),
@@ -471,6 +473,22 @@ def render_reference(volume: np.ndarray, density_scale: float, camera: PinholeCa
     cam, rc = camera._c(), cfg._c()
     _check(_lib.tv_render_regular(v.ctypes.data_as(_F), nx, ny, nz, float(density_scale), C.byref(cam), C.byref(rc),
                                   int(device), C.byref(fb), C.byref(st)))
+    return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
+
+
+def render_reference_dev(density_dev: int, shape, density_scale: float, camera: PinholeCamera, cfg: RenderConfig,
+                         device: int = 0) -> ImageAccumulator:
+    """render_reference with the density already in HBM (raw device pointer, shape = (nz, ny, nx))."""
+    nz, ny, nx = shape
+    w, h = int(camera.width), int(camera.height)
+    s = np.zeros(w * h * 3)
+    sq = np.zeros(w * h * 3)
+    cnt = np.zeros(w * h, np.uint32)
+    fb = _Framebuffer(s.ctypes.data_as(_D), sq.ctypes.data_as(_D), cnt.ctypes.data_as(_U32))
+    st = _RenderStats()
+    cam, rc = camera._c(), cfg._c()
+    _check(_lib.tv_render_regular_dev(density_dev, nx, ny, nz, float(density_scale), C.byref(cam), C.byref(rc),
+                                      int(device), C.byref(fb), C.byref(st)))
     return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
 
 

@@ -987,10 +987,10 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     };
 
     // initial capacity guess: grows geometrically as needed
-    TRY(grow_tets(std::max<size_t>(1 << 16, nvox / 4)));
+    TRY(grow_tets(std::min<size_t>(std::max<size_t>(1 << 16, nvox / 4), size_t(1) << 24)));
     CK(cudaMemcpy(tets_b.p, ht.data(), ht.size() * sizeof(tv_tet), cudaMemcpyHostToDevice), "roots H2D");
     {
-        const size_t need_v = std::max<size_t>(1 << 15, nvox / 16);
+        const size_t need_v = std::min<size_t>(std::max<size_t>(1 << 15, nvox / 16), size_t(1) << 22);
         TRY(ensure(verts_b, need_v * sizeof(uint4)));
         CK(cudaMemcpy(verts_b.p, hv.data(), hv.size() * sizeof(uint4), cudaMemcpyHostToDevice), "verts H2D");
         TRY(grow_verts(need_v));

@@ -191,6 +191,9 @@ int workspace(int device, Workspace*& out) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace), kTraceThreads,
                                                       0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
+        if (env_int("TV_VERBOSE", 0))
+            std::fprintf(stderr, "tetvol_b200: trace kernel minb=%d, %d blocks/SM resident, %d blocks\n", minb, per_sm,
+                         w.trace_blocks);
     }
     out = &w;
     return TV_OK;

@@ -180,9 +180,9 @@ int validate_render_cfg(const tv_render_config* r);  // tv_capi.cu
 
 using namespace tvb;
 
-extern "C" int tv_render_regular(const float* density, int32_t nx, int32_t ny, int32_t nz, double density_scale,
-                                 const tv_camera* camera, const tv_render_config* cfg, int device, tv_framebuffer* out,
-                                 tv_render_stats* stats) {
+static int render_regular(const float* density, bool on_device, int32_t nx, int32_t ny, int32_t nz,
+                          double density_scale, const tv_camera* camera, const tv_render_config* cfg, int device,
+                          tv_framebuffer* out, tv_render_stats* stats) {
     if (!density) return set_error(TV_ERR_ARG, "density is null");
     if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR, "volume dimensions must be positive");
     if (density_scale < 0.0) return set_error(TV_ERR, "density scale must be non-negative");  // regular_grid.cpp:123
@@ -216,20 +216,20 @@ extern "C" int tv_render_regular(const float* density, int32_t nx, int32_t ny, i
     auto cleanup = [&]() {
         cudaFree(raw), cudaFree(dens), cudaFree(rad), cudaFree(sum), cudaFree(sum_sq), cudaFree(counts), cudaFree(st);
     };
-    e = cudaMalloc(&raw, nvox * sizeof(float));
+    e = on_device ? cudaSuccess : cudaMalloc(&raw, nvox * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&dens, nvox * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&rad, units * 32 * ns * 3 * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&sum, npx * 3 * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&sum_sq, npx * 3 * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&counts, npx * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&st, 3 * sizeof(uint64_t));
-    if (e == cudaSuccess) e = cudaMemcpy(raw, density, nvox * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !on_device) e = cudaMemcpy(raw, density, nvox * sizeof(float), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(st, 0, 3 * sizeof(uint64_t));
     if (e != cudaSuccess) {
         cleanup();
         return cuda_status(e, "render_regular setup");
     }
-    scale_kernel<<<148 * 8, 256>>>(raw, dens, nvox, density_scale);
+    scale_kernel<<<148 * 8, 256>>>(on_device ? density : raw, dens, nvox, density_scale);
     DdaGrid G{dens, {nx, ny, nz}};
     RenderOut ro{sum, sum_sq, counts, st};
     cudaEvent_t e0, e1;
@@ -274,4 +274,16 @@ extern "C" int tv_render_regular(const float* density, int32_t nx, int32_t ny, i
         stats->seconds = ms * 1e-3;
     }
     return TV_OK;
+}
+
+extern "C" int tv_render_regular(const float* density, int32_t nx, int32_t ny, int32_t nz, double density_scale,
+                                 const tv_camera* camera, const tv_render_config* cfg, int device, tv_framebuffer* out,
+                                 tv_render_stats* stats) {
+    return render_regular(density, false, nx, ny, nz, density_scale, camera, cfg, device, out, stats);
+}
+
+extern "C" int tv_render_regular_dev(const float* density_dev, int32_t nx, int32_t ny, int32_t nz,
+                                     double density_scale, const tv_camera* camera, const tv_render_config* cfg,
+                                     int device, tv_framebuffer* out, tv_render_stats* stats) {
+    return render_regular(density_dev, true, nx, ny, nz, density_scale, camera, cfg, device, out, stats);
 }

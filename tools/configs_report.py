@@ -1,0 +1,105 @@
+"""Measure the BASELINE configs beyond the bench line (C2 threshold sweep, C3/C5
+at 512^3, C4 build at 1024^3) on one B200; prints one JSON object per row.
+
+    python tools/configs_report.py [rows...]   rows: c2 c3 c5 c4 (default: all)
+"""
+import json
+import sys
+import time
+
+sys.path.insert(0, ".")
+import torch
+
+import paper_2506_11510_b200 as tv
+
+CAM = dict(position=(0.5, 0.5, -1.2), forward=(0.0, 0.0, 1.0), up=(0.0, 1.0, 0.0), vfov_degrees=40.0, width=1024,
+           height=1024)
+
+
+def field(n):
+    vol = torch.empty(n ** 3, dtype=torch.float32, device="cuda")
+    tv.generate_volume_dev("cloud", n, vol.data_ptr())
+    return vol
+
+
+def build(vol, n, thr, ml, camera=True):
+    cam = tv.PinholeCamera(**CAM) if camera else None
+    g, st = tv.build_adaptive_grid_dev(vol.data_ptr(), (n, n, n), tv.BuildConfig(thr, ml, camera, 1.0, 16.0), cam)
+    torch.cuda.synchronize()
+    return g, st
+
+
+def render(g, spp=32, frames=2):
+    cam = tv.PinholeCamera(**CAM)
+    rc = tv.RenderConfig(spp=spp, max_bounces=64, seed=0)
+    best = None
+    for _ in range(frames):
+        img = tv.render(g, cam, rc)
+        if best is None or img.seconds < best.seconds:
+            best = img
+    return best
+
+
+def row(**kw):
+    print(json.dumps(kw), flush=True)
+
+
+def c2():
+    vol = field(256)
+    for thr in [0.15, 1.0, 2.0, 4.0]:
+        g, st = build(vol, 256, thr, 24)
+        img = render(g)
+        i = g.info()
+        row(config="C2", field="cloud 256^3 + camera", threshold=thr, max_level=24, leaves=i["n_leaves"],
+            tets=i["n_tets"], build_s=st.seconds, rounds=st.rounds, ms_per_frame=img.seconds * 1e3,
+            samples_per_s=img.paths_traced / img.seconds, cells_per_path=img.cells_visited / img.paths_traced,
+            tet_steps_per_s=img.cells_visited / img.seconds)
+        g.close()
+
+
+def c3_c5():
+    vol = field(512)
+    res = {}
+    for thr in [0.15, 2.0]:
+        g, st = build(vol, 512, thr, 27)
+        img = render(g)
+        i = g.info()
+        res[thr] = img
+        row(config="C3 (1 GPU, 32 spp)", field="cloud 512^3 + camera", threshold=thr, max_level=27,
+            leaves=i["n_leaves"], tets=i["n_tets"], build_s=st.seconds, ms_per_frame_32spp=img.seconds * 1e3,
+            ms_per_frame_1024spp_extrapolated=img.seconds * 1e3 * 32, cells_per_path=img.cells_visited / img.paths_traced,
+            tet_steps_per_s=img.cells_visited / img.seconds)
+        g.close()
+    cam = tv.PinholeCamera(**CAM)
+    rc = tv.RenderConfig(spp=32, max_bounces=64, seed=0)
+    reg = tv.render_reference_dev(vol.data_ptr(), (512, 512, 512), 16.0, cam, rc)
+    for thr, img in res.items():
+        row(config="C5", field="cloud 512^3", regular_ms=reg.seconds * 1e3,
+            regular_cells_per_path=reg.cells_visited / reg.paths_traced, tet_threshold=thr,
+            tet_ms=img.seconds * 1e3, tet_cells_per_path=img.cells_visited / img.paths_traced,
+            speedup_tet_vs_regular=reg.seconds / img.seconds)
+
+
+def c4():
+    vol = field(1024)
+    for thr in [4.0, 2.0]:
+        t = time.time()
+        g, st = build(vol, 1024, thr, 30, camera=False)
+        i = g.info()
+        row(config="C4", field="cloud 1024^3 (no camera)", threshold=thr, max_level=30, leaves=i["n_leaves"],
+            tets=i["n_tets"], build_s_device=st.seconds, wall_s=time.time() - t, rounds=st.rounds,
+            closure_passes=st.closure_passes, leaves_per_s=i["n_leaves"] / st.seconds,
+            voxel_visits=st.voxel_visits, voxel_visits_per_s=st.voxel_visits / st.seconds, max_depth=st.max_depth)
+        g.close()
+        if i["n_leaves"] > 45e6:
+            break
+
+
+if __name__ == "__main__":
+    rows = sys.argv[1:] or ["c2", "c3", "c4"]
+    if "c2" in rows:
+        c2()
+    if "c3" in rows or "c5" in rows:
+        c3_c5()
+    if "c4" in rows:
+        c4()
