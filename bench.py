@@ -179,6 +179,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", action="store_true", help="use the multi-GPU tile gather path even on one rank")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -193,7 +194,8 @@ def main():
     from paper_2506_11510_b200 import sharding
 
     torch.cuda.set_device(local)
-    if world > 1:
+    multi = world > 1 or args.gather  # --gather exercises the NCCL tile path even on one rank
+    if multi:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local
 
@@ -226,7 +228,7 @@ def main():
                         stats.data_ptr(), sh)
         if timed:
             k_end[i].record(stream)
-        if world > 1:
+        if multi:
             tv.tile_pack(sum_.data_ptr(), packed.data_ptr(), W_IMG, H_IMG, rank, world, 3, sh)
             with torch.cuda.stream(stream):
                 dist.all_gather_into_tensor(gathered, packed)
@@ -238,7 +240,7 @@ def main():
         step(i)
     stream.synchronize()
     stats.zero_()
-    if world > 1:
+    if multi:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
@@ -258,7 +260,7 @@ def main():
     trace_ms = timing["trace_ms"]
     st = stats.cpu().numpy()
     cells_rank = int(st[0]) // args.steps
-    if world > 1:
+    if multi:
         red = torch.tensor([ms, kern_ms, float(cells_rank)], dtype=torch.float64, device="cuda")
         mx = red.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
@@ -274,7 +276,7 @@ def main():
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
-    if world == 1:
+    if not multi:
         hs = torch.empty(npx * 3, dtype=torch.float64, pin_memory=True).numpy()
         hq = torch.empty(npx * 3, dtype=torch.float64, pin_memory=True).numpy()
         hc = torch.empty(npx, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
@@ -348,11 +350,11 @@ def main():
                        "build_s_device": bst.seconds},
             "tet_steps_per_s": cells_frame / (ms * 1e-3), "cells_per_path": cells_frame / samples,
             "ms_per_frame": ms, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "gpu_launches": (timing["launches"] + (1 + world if world > 1 else 0)) * args.steps,
+            "gpu_launches": (timing["launches"] + (1 + world if multi else 0)) * args.steps,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
 
