@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtetvol_b200.so")
+LIB_PATH = os.environ.get("TETVOL_B200_LIB") or os.path.join(_HERE, "_lib", "libtetvol_b200.so")
 NO_TET = 0xFFFFFFFF
 
 if not os.path.exists(LIB_PATH):
