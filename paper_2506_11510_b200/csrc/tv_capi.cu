@@ -147,7 +147,7 @@ struct Workspace {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int trace_blocks = 0, sms = 0;
     TraceFn trace = nullptr;
-    uint32_t regen_min = 8, scatter_min = 8, prefetch = 0, order = 0;
+    uint32_t regen_min = 8, scatter_min = 8, order = 0;
     cudaEvent_t tev[4 * 8] = {};  // per-batch kernel boundaries of the last frame
     int n_timed = 0, n_launches = 0;
 };
@@ -178,11 +178,10 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaEventCreate(&w.ev1), "event create");
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
         // tuning knobs (defaults are the measured best on B200)
-        const int minb = env_int("TV_TRACE_MINB", 4);
-        w.trace = trace_variant(minb);
+        const int maxreg = env_int("TV_TRACE_MAXREG", 128);
+        w.trace = trace_variant(maxreg);
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 1));
-        w.prefetch = static_cast<uint32_t>(env_int("TV_PREFETCH", 0));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
         int per_sm = 1;
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -192,7 +191,7 @@ int workspace(int device, Workspace*& out) {
                                                       0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
         if (env_int("TV_VERBOSE", 0))
-            std::fprintf(stderr, "tetvol_b200: trace kernel minb=%d, %d blocks/SM resident, %d blocks\n", minb, per_sm,
+            std::fprintf(stderr, "tetvol_b200: trace kernel maxreg=%d, %d blocks/SM resident, %d blocks\n", maxreg, per_sm,
                          w.trace_blocks);
     }
     out = &w;
@@ -240,7 +239,6 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.first = s0 == 0 ? 1u : 0u;
         B.regen_min = w.regen_min;
         B.scatter_min = w.scatter_min;
-        B.prefetch = w.prefetch;
         B.order = w.order;
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
         if (ev) TV_CK(cudaEventRecord(ev[0], st), "event");

@@ -75,16 +75,17 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
     uint32_t codes = 0;
     for (int f = 0; f < 4; ++f) {
         const uint32_t nb = tt.neighbors[f];
-        r.w[f] = nb == kNone ? kNone : tet2leaf[nb];
+        const uint32_t id = static_cast<uint32_t>(tt.normal_ids[f]) & 31u;
+        r.w[f] = (nb == kNone ? kNoLeaf : tet2leaf[nb]) | (id << 27);
         // exit_face reads vertex verts[(f+1)&3] of face f (tracer.cpp:152)
         const uint32_t code = face_code(tt.normal_ids[f]);
         const uint4 q = verts[tt.verts[(f + 1) & 3]];
         const uint32_t qq[3] = {q.x, q.y, q.z};
         r.w[4 + 2 * f] = __float_as_uint(static_cast<float>(qq[code & 3u]) * 0x1.0p-24f);
         r.w[5 + 2 * f] = __float_as_uint(static_cast<float>(qq[(code >> 2) & 3u]) * 0x1.0p-24f);
-        codes |= (static_cast<uint32_t>(tt.normal_ids[f]) & 31u) << (5 * f);
+        codes |= leaf_code6(face_code(id & ~1u)) << (6 * f);
     }
-    r.w[12] = codes | (static_cast<uint32_t>(tt.mask & 7u) << 20);
+    r.w[12] = codes | (static_cast<uint32_t>(tt.mask & 7u) << 24);
     mask[L] = tt.mask;
     r.w[13] = __float_as_uint(tt.density);
     r.w[14] = __float_as_uint(tt.temperature);
@@ -200,6 +201,11 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     } while (0)
 #define CK(x, what) TRY(cuda_status((x), what))
 
+    if (g.n_leaves >= kNoLeaf) {
+        return set_error(TV_ERR_GRID, "grid has " + std::to_string(g.n_leaves) +
+                                          " leaves; the traversal layout holds at most " +
+                                          std::to_string(kNoLeaf - 1));
+    }
     TRY(dalloc(&keys, nt, scratch_bytes));
     TRY(dalloc(&keys_sorted, nt, scratch_bytes));
     TRY(dalloc(&ids, nt, scratch_bytes));

@@ -163,7 +163,7 @@ __global__ void march_kernel(GridView G, const tv_ray* __restrict__ rays, uint64
                 }
                 const double t_exit = dmax(probe + t, seg_start);
                 const bool clip = t_exit >= tmax;
-                const uint32_t nb = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot);
+                const uint32_t nb = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot) & kLeafIdxMask;
                 if (pass && base + k < cap) {
                     tv_segment sgm;
                     sgm.cell = G.leaf2tet[cell];
@@ -173,7 +173,7 @@ __global__ void march_kernel(GridView G, const tv_ray* __restrict__ rays, uint64
                     out[base + k] = sgm;
                 }
                 ++k;
-                if (clip || nb == kNone) break;
+                if (clip || nb == kNoLeaf) break;
                 rec = load_leaf(G.leaves, nb);
                 cell = nb;
                 seg_start = t_exit;

@@ -7,8 +7,10 @@
 
 namespace tvb {
 
-constexpr int kTraceThreads = 128;
-constexpr int kTraceMinBlocks = 5;
+#ifndef TV_TRACE_THREADS
+#define TV_TRACE_THREADS 128
+#endif
+constexpr int kTraceThreads = TV_TRACE_THREADS;
 constexpr uint32_t kChunk = 64;               // paths a warp claims per queue atomic
 constexpr uint32_t kInvalidPixel = 0xfffffffeu;
 constexpr uint64_t kMaxBatchPaths = 1ull << 26;
@@ -25,7 +27,6 @@ struct Batch {
     uint32_t n_paths;
     uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
     uint32_t regen_min, scatter_min;  // warp-batching thresholds of the trace loop
-    uint32_t prefetch;                // 0 none, 1 neighbour records to L1, 2 to L2
     uint32_t order;                   // path id order (see path_id in tv_trace.cu)
 };
 
