@@ -17,6 +17,8 @@
  *   tv_locate_points    <- TetGrid::locate_point (tet_grid.hpp:166)
  *   tv_render_regular   <- render_reference(RegularGrid::from_volume(vol, s),
  *                          camera, cfg) (regular_grid.hpp:66-67)
+ *   tv_grid_save        <- save_grid(grid, path) (builder.hpp:59)
+ *   tv_grid_load        <- load_grid(path) (builder.hpp:60)
  *
  * Conventions: no C++ exception crosses this boundary; every function returns
  * a tv_status (0 = TV_OK) and tv_last_error() holds a thread-local message.
@@ -48,7 +50,9 @@ typedef enum {
     TV_ERR_OUTSIDE = 5, /* OutsideGrid (tet_grid.hpp:33-35)                           */
     TV_ERR_CUDA = 6,    /* no device, launch or copy failure                          */
     TV_ERR_OOM = 7,     /* device allocation failed                                   */
-    TV_ERR_ARG = 8      /* null pointer / size mismatch at the ABI                    */
+    TV_ERR_ARG = 8,     /* null pointer / size mismatch at the ABI                    */
+    TV_ERR_FORMAT = 9,  /* FormatError: malformed .tgrid (builder.cpp:184-293)          */
+    TV_ERR_IO = 10      /* IoError: cannot open / write a file                        */
 } tv_status;
 
 /* Reference Vertex (tet_grid.hpp:41-49): fixed point, position = q / 2^24. */
@@ -177,6 +181,12 @@ int tv_grid_upload(const tv_vertex* vertices, uint64_t n_vertices, const tv_tet*
 int tv_grid_download(const tv_grid* g, tv_vertex* vertices, tv_tet* tets, uint32_t roots[24]);
 int tv_grid_get_info(const tv_grid* g, tv_grid_info* out);
 void tv_grid_free(tv_grid* g);
+/* The reference's TGRD v1 file (save_grid / load_grid, builder.cpp:184-293),
+ * byte-identical to save_grid of the same pools; records are packed and
+ * unpacked on the device. load applies load_grid's checks and messages
+ * (TV_ERR_FORMAT) and assembles with max_level 48 as load_grid does. */
+int tv_grid_save(const tv_grid* g, const char* path);
+int tv_grid_load(const char* path, int device, tv_grid** out);
 
 /* -- LEB build on the GPU --------------------------------------------------- */
 /* density/temperature/albedo: nx*ny*nz floats, x fastest (volume.hpp:41-43);

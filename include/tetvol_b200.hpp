@@ -40,6 +40,8 @@ inline void check(int rc) {
         case TV_ERR_CAMERA: throw CameraError(msg);
         case TV_ERR_GRID: throw GridError(msg);
         case TV_ERR_OUTSIDE: throw OutsideGrid(msg);
+        case TV_ERR_FORMAT: throw FormatError(msg);
+        case TV_ERR_IO: throw IoError(msg);
         default: throw std::runtime_error("tetvol_b200: " + msg);
     }
 }
@@ -127,6 +129,14 @@ public:
 private:
     tv_grid* h_ = nullptr;
 };
+
+// builder.hpp:59-60 — the reference's TGRD v1 file, packed / unpacked on the device
+inline void save_grid(const DeviceGrid& grid, const std::string& path) { check(tv_grid_save(grid.handle(), path.c_str())); }
+inline DeviceGrid load_grid_device(const std::string& path, int device = 0) {
+    tv_grid* h = nullptr;
+    check(tv_grid_load(path.c_str(), device, &h));
+    return DeviceGrid(h);
+}
 
 // tracer.hpp:84-85
 inline ImageAccumulator render(const DeviceGrid& grid, const PinholeCamera& camera, const RenderConfig& cfg,

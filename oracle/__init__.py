@@ -195,6 +195,7 @@ class Checker:
             f("grid_uniform", _P, C.c_int)
             f("grid_load", _P, C.c_char_p)
             f("grid_save", C.c_int, _P, C.c_char_p)
+            f("grid_set_payload", None, _P, C.c_uint32, C.c_float, C.c_float, C.c_float, C.c_uint32)
             f("trace_sample", None, _P, C.POINTER(Camera), C.POINTER(RenderCfg), C.c_int, C.c_int, C.c_int, _D, _U64)
 
     def fn(self, name):

@@ -56,8 +56,16 @@ class CudaError(TetvolError):
     """No usable CUDA device, or a launch/copy failed."""
 
 
+class FormatError(TetvolError):
+    """errors.hpp: malformed .tgrid (builder.cpp:184-293)"""
+
+
+class IoError(TetvolError):
+    """errors.hpp: a file cannot be opened or written"""
+
+
 _ERRS = {1: TetvolError, 2: ConfigError, 3: CameraError, 4: GridError, 5: OutsideGrid, 6: CudaError,
-         7: CudaError, 8: ValueError}
+         7: CudaError, 8: ValueError, 9: FormatError, 10: IoError}
 
 
 def _check(rc: int):
@@ -127,6 +135,8 @@ _sig("tv_grid_upload", C.c_int, _P, C.c_uint64, _P, C.c_uint64, _U32, C.c_int32,
 _sig("tv_grid_download", C.c_int, _P, _P, _P, _U32)
 _sig("tv_grid_get_info", C.c_int, _P, C.POINTER(_GridInfo))
 _sig("tv_grid_free", None, _P)
+_sig("tv_grid_save", C.c_int, _P, C.c_char_p)
+_sig("tv_grid_load", C.c_int, C.c_char_p, C.c_int, C.POINTER(_P))
 _sig("tv_build", C.c_int, _F, _F, _F, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_BuildConfig), C.POINTER(_Camera),
      C.c_int, C.POINTER(_P), C.POINTER(_BuildStats))
 _sig("tv_build_dev", C.c_int, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_BuildConfig),
@@ -317,6 +327,17 @@ class TetGrid:
         _check(_lib.tv_grid_download(self.handle, v.ctypes.data_as(_P), t.ctypes.data_as(_P), r.ctypes.data_as(_U32)))
         return v, t, r
 
+    def save(self, path) -> None:
+        """save_grid (builder.hpp:59): the reference's TGRD v1 file, packed on the device."""
+        _check(_lib.tv_grid_save(self.handle, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path, device: int = 0) -> "TetGrid":
+        """load_grid (builder.hpp:60): checks and messages as the reference, unpacked on the device."""
+        h = _P()
+        _check(_lib.tv_grid_load(os.fsencode(path), int(device), C.byref(h)))
+        return cls(h)
+
     def close(self):
         if getattr(self, "_h", None):
             _lib.tv_grid_free(self._h)
@@ -492,8 +513,19 @@ def render_reference_dev(density_dev: int, shape, density_scale: float, camera: 
     return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
 
 
+def save_grid(grid: TetGrid, path) -> None:
+    """builder.hpp:59"""
+    grid.save(path)
+
+
+def load_grid(path, device: int = 0) -> TetGrid:
+    """builder.hpp:60"""
+    return TetGrid.load(path, device)
+
+
 __all__ = [
-    "BuildConfig", "BuildStats", "CameraError", "ConfigError", "CudaError", "GridError", "ImageAccumulator",
+    "BuildConfig", "BuildStats", "CameraError", "ConfigError", "CudaError", "FormatError", "GridError",
+    "ImageAccumulator", "IoError", "load_grid", "save_grid",
     "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
     "build_adaptive_grid", "build_adaptive_grid_dev", "device_count", "generate_volume_dev", "locate_points",
     "march_segments", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",

@@ -30,6 +30,15 @@ int cuda_status(cudaError_t e, const char* what) {
     return set_error(TV_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+int use_device(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return set_error(TV_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= n) return set_error(TV_ERR_CUDA, "device index out of range");
+    return cuda_status(cudaSetDevice(device), "cudaSetDevice");
+}
+
 namespace {
 
 #define TV_CK(x, what)                                  \
@@ -121,15 +130,6 @@ RenderParams make_params(const tv_render_config* r) {
     p.env[0] = r->environment[0], p.env[1] = r->environment[1], p.env[2] = r->environment[2];
     p.emission_scale = r->emission_scale;
     return p;
-}
-
-int use_device(int device) {
-    int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess || n == 0)
-        return set_error(TV_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
-    if (device < 0 || device >= n) return set_error(TV_ERR_CUDA, "device index out of range");
-    return cuda_status(cudaSetDevice(device), "cudaSetDevice");
 }
 
 // Per-device workspace reused across frames (no cudaMalloc in the per-frame

@@ -77,6 +77,8 @@ void free_grid(DeviceGrid& g);
 // thread-local error plumbing for the C ABI
 int set_error(int code, const std::string& msg);
 int cuda_status(cudaError_t e, const char* what);
+// selects `device` (TV_ERR_CUDA when there is none)
+int use_device(int device);
 // camera.cpp:12-45 on the host (optional frustum planes for the build)
 int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]);
 

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "tetvol_b200.hpp"
@@ -24,6 +25,29 @@ static DenseVolume blob(int n) {
                 d[v.index(i, j, k)] = static_cast<float>(t * t);
             }
     return v;
+}
+
+// field-wise (padding bytes are unspecified)
+static bool same_tets(const TetGrid& a, const TetGrid& b) {
+    if (a.tet_count() != b.tet_count() || a.vertex_count() != b.vertex_count()) return false;
+    for (size_t v = 0; v < a.vertex_count(); ++v)
+        for (int k = 0; k < 3; ++k)
+            if (a.vertices()[v].q[k] != b.vertices()[v].q[k]) return false;
+    for (size_t t = 0; t < a.tet_count(); ++t) {
+        const Tet &x = a.tets()[t], &y = b.tets()[t];
+        for (int k = 0; k < 4; ++k)
+            if (x.verts[k] != y.verts[k] || x.neighbors[k] != y.neighbors[k] || x.normal_ids[k] != y.normal_ids[k])
+                return false;
+        if (x.children[0] != y.children[0] || x.children[1] != y.children[1] || x.parent != y.parent ||
+            x.level != y.level || x.payload.mask != y.payload.mask ||
+            std::memcmp(&x.payload.density, &y.payload.density, 4) ||
+            std::memcmp(&x.payload.temperature, &y.payload.temperature, 4) ||
+            std::memcmp(&x.payload.albedo, &y.payload.albedo, 4))
+            return false;
+    }
+    for (int r = 0; r < 24; ++r)
+        if (a.roots()[r] != b.roots()[r]) return false;
+    return true;
 }
 
 static std::vector<std::array<uint32_t, 12>> leaf_set(const TetGrid& g) {
@@ -98,6 +122,26 @@ int main() {
             REQUIRE(want[k].t_enter == segs[i][k].t_enter);
             REQUIRE(want[k].t_exit == segs[i][k].t_exit);
         }
+    }
+
+    // .tgrid: our device-packed file loads in the reference with the same pools,
+    // and the reference's file loads on the device with the same pools
+    {
+        const std::string p1 = "/tmp/shim_drop_in_a.tgrid", p2 = "/tmp/shim_drop_in_b.tgrid";
+        b200::save_grid(dg, p1);
+        TetGrid back = load_grid(p1);
+        REQUIRE(back.tet_count() == ref.tet_count() && back.vertex_count() == ref.vertex_count());
+        REQUIRE(same_tets(back, ref));
+        save_grid(ref, p2);
+        TetGrid dev_back = b200::load_grid_device(p2).download();
+        REQUIRE(same_tets(dev_back, ref));
+        try {
+            b200::load_grid_device("/tmp/shim_drop_in_missing.tgrid");
+            REQUIRE(false);
+        } catch (const IoError&) {
+        }
+        std::remove(p1.c_str());
+        std::remove(p2.c_str());
     }
 
     // exceptions map back to the reference types

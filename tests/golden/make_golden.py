@@ -14,6 +14,7 @@ import hashlib
 import json
 import os
 import sys
+import tempfile
 
 import numpy as np
 
@@ -115,6 +116,11 @@ def main():
     gold["c1_grid"] = {"counts": g.counts(), "stats": {k: v for k, v in st.items() if k != "seconds"},
                        "sha": h(p.vq, p.tets, p.roots),
                        "sum_leaf_density": bits(float(p.tets["density"][lm].astype(np.float64).sum()))}
+    with tempfile.TemporaryDirectory() as td:  # save_grid bytes (builder.cpp:210-235)
+        fn = os.path.join(td, "c1.tgrid")
+        assert R.fn("grid_save")(g.h, fn.encode()) == 0, R.err()
+        raw = open(fn, "rb").read()
+    gold["c1_tgrid"] = {"bytes": len(raw), "sha256": hashlib.sha256(raw).hexdigest()}
     rc = O.render_cfg(spp=4, max_bounces=2, seed=0)
     img = g.render(cam, rc, 0)
     gold["c1_render"] = {"cells_visited": img["cells_visited"], "degenerate_paths": img["degenerate_paths"],

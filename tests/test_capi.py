@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
 
     lib = ctypes.CDLL(tv.LIB_PATH)
     syms = declared_symbols()
-    assert len(syms) >= 18
+    assert len(syms) >= 22
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
     assert "sm_100a" in tv.version()
@@ -93,3 +93,30 @@ def test_upload_rejects_corrupt_pools_like_load_grid():
         tv.TetGrid.upload(p.vq, bad, p.roots)
     with pytest.raises(ValueError):
         tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots[:23])
+
+
+def test_tgrid_header_errors_before_device(tmp_path):
+    """load_grid's header checks (builder.cpp:240-247) run before any device work."""
+    import paper_2506_11510_b200 as tv
+
+    cases = {"magic": b"TGRX" + bytes(12), "version": b"TGRD" + (2).to_bytes(4, "little") + bytes(8),
+             "count": b"TGRD" + (1).to_bytes(4, "little") + (7).to_bytes(8, "little"), "empty": b""}
+    want = {"magic": "not a TGRD file: ", "version": "unsupported TGRD version", "count": "bad vertex count",
+            "empty": "not a TGRD file: "}
+    for k, raw in cases.items():
+        fn = tmp_path / f"{k}.tgrid"
+        fn.write_bytes(raw)
+        with pytest.raises(tv.FormatError) as e:
+            tv.load_grid(fn)
+        assert str(e.value).startswith(want[k])
+    with pytest.raises(tv.IoError, match="cannot open"):
+        tv.load_grid(tmp_path / "missing.tgrid")
+    if tv.device_count() == 0:  # a valid file still needs the device: no CPU fallback
+        import oracle as O
+        from oracle.tgrid import tgrid_bytes
+
+        p = O.init_roots(O.c_oracle()).pools()
+        fn = tmp_path / "roots.tgrid"
+        fn.write_bytes(tgrid_bytes(p.vq, p.tets, p.roots))
+        with pytest.raises(tv.CudaError):
+            tv.load_grid(fn)

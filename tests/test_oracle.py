@@ -256,8 +256,6 @@ def test_step_and_noise_builds_vs_reference(chk):
 def test_regular_grid_vs_reference(chk):
     vol = O.gen_volume("cloud", 24)
     rays = O.random_cube_rays(3, 17, 400)
-    for lib in (chk, ref):
-        pass
     out = []
     for lib in (chk, ref):
         off = np.zeros(401, np.uint64)
@@ -273,3 +271,28 @@ def test_regular_grid_vs_reference(chk):
         out.append((cells, t0, t1, off))
     for u, v in zip(*out):
         assert np.array_equal(u, v)
+
+
+def test_tgrid_restatement_golden(c1):
+    """oracle/tgrid.py restates save_grid; pinned to the reference's C1 file bytes."""
+    from oracle.tgrid import tgrid_bytes
+
+    p = c1[1].pools()
+    raw = tgrid_bytes(p.vq, p.tets, p.roots)
+    assert len(raw) == GOLD["c1_tgrid"]["bytes"]
+    assert hashlib.sha256(raw).hexdigest() == GOLD["c1_tgrid"]["sha256"]
+
+
+@needs_ref
+def test_tgrid_restatement_matches_reference(tmp_path):
+    from oracle.tgrid import tgrid_bytes
+
+    cam = O.camera((0.5, 0.5, -2), (0, 0, 1), (0, 1, 0), 16, 128, 128)
+    vol = O.gen_volume("blob", 24)
+    temp = (vol * 0.7).astype(np.float32)
+    alb = np.full_like(vol, 0.5)
+    for g in [O.fuzzed(ref, 200, 5), O.build(ref, vol, O.build_cfg(0.15, 9, True, 0.5, 1.0), cam, temp, alb)[0]]:
+        fn = str(tmp_path / "g.tgrid")
+        assert ref.fn("grid_save")(g.h, fn.encode()) == 0
+        p = g.pools()
+        assert tgrid_bytes(p.vq, p.tets, p.roots) == open(fn, "rb").read()
