@@ -52,7 +52,9 @@ typedef enum {
     TV_ERR_OOM = 7,     /* device allocation failed                                   */
     TV_ERR_ARG = 8,     /* null pointer / size mismatch at the ABI                    */
     TV_ERR_FORMAT = 9,  /* FormatError: malformed .tgrid (builder.cpp:184-293)          */
-    TV_ERR_IO = 10      /* IoError: cannot open / write a file                        */
+    TV_ERR_IO = 10,     /* IoError: cannot open / write a file                        */
+    TV_ERR_VOLUME = 11, /* VolumeError / UnknownChannel (volume.hpp:13-18)            */
+    TV_ERR_IMAGE = 12   /* ImageError: PFM I/O (image.cpp)                            */
 } tv_status;
 
 /* Reference Vertex (tet_grid.hpp:41-49): fixed point, position = q / 2^24. */
@@ -156,6 +158,16 @@ typedef struct {
 } tv_segment;
 
 typedef struct tv_grid tv_grid;
+typedef struct tv_volume tv_volume;
+
+/* cmd_compare's image metrics (cli.cpp:499-531). outlier_fraction < 0 when no
+ * variance images were given (the reference reports null). */
+typedef struct {
+    double rmse;
+    double max_abs_diff;
+    double outlier_fraction;
+    uint64_t outliers;
+} tv_compare_stats;
 
 typedef struct {
     uint64_t n_vertices;
@@ -214,6 +226,13 @@ int tv_render(const tv_grid* g, const tv_camera* camera, const tv_render_config*
 int tv_render_tiles(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg, int32_t rank,
                     int32_t n_ranks, double* sum_dev, double* sum_sq_dev, uint32_t* counts_dev, uint64_t* stats_dev,
                     void* stream);
+/* Progressive accumulation: renders samples [first_sample, first_sample +
+ * cfg->spp) of this rank's tiles and ADDS them to the device accumulators in
+ * sample order (first_sample == 0 initialises them). Frames covering [0, N)
+ * leave exactly the framebuffer of one N-spp render (bit-identical). */
+int tv_render_accumulate(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg,
+                         int32_t first_sample, int32_t rank, int32_t n_ranks, double* sum_dev, double* sum_sq_dev,
+                         uint32_t* counts_dev, uint64_t* stats_dev, void* stream);
 /* Device time (ms) of the last frame rendered on `device`, per kernel:
  * out[0] start (camera rays + locate), out[1] trace, out[2] accumulate;
  * out[3] = number of kernel launches of that frame. Synchronises on it. */
@@ -226,6 +245,44 @@ int tv_tile_pack(const void* frame_dev, void* packed_dev, int32_t width, int32_t
                  int32_t n_ranks, int32_t elem_words, void* stream);
 int tv_tile_unpack(const void* packed_dev, void* frame_dev, int32_t width, int32_t height, int32_t rank,
                    int32_t n_ranks, int32_t elem_words, void* stream);
+
+/* -- volumes in HBM (DenseVolume, volume.hpp:19-58; .dvol, volume.cpp:84-138) -- */
+/* create: a zero "density" channel (volume.hpp:25); dims in [1, 4096].       */
+int tv_volume_create(int32_t nx, int32_t ny, int32_t nz, int device, tv_volume** out);
+int tv_volume_load(const char* path, int device, tv_volume** out); /* load_dvol */
+int tv_volume_save(const tv_volume* v, const char* path);          /* save_dvol */
+void tv_volume_free(tv_volume* v);
+int tv_volume_get_info(const tv_volume* v, int32_t dims[3], int32_t* n_channels);
+int tv_volume_channel_name(const tv_volume* v, int32_t index, char* buf, int32_t cap);
+int tv_volume_channel_dev(const tv_volume* v, const char* name, float** out_dev);
+int tv_volume_add_channel(tv_volume* v, const char* name);         /* zero-filled */
+int tv_volume_upload(tv_volume* v, const char* name, const float* in);
+int tv_volume_download(const tv_volume* v, const char* name, float* out);
+/* cmd_gen on the device (cli.cpp:349-380): density of a procedural kind
+ * (as tv_generate_volume_dev), temperature = clamp(density, 0, 1), constant albedo */
+int tv_volume_generate(tv_volume* v, int32_t kind, double value);
+int tv_volume_add_temperature(tv_volume* v);
+int tv_volume_add_albedo(tv_volume* v, double albedo);
+/* build_adaptive_grid(DenseVolume, ...) with the volume's density and
+ * optional temperature / albedo channels (builder.cpp:164-182) */
+int tv_build_volume(const tv_volume* v, const tv_build_config* cfg, const tv_camera* camera, tv_grid** out,
+                    tv_build_stats* stats);
+
+/* -- images (image.cpp:33-101) and compare (cli.cpp:487-531) ------------------ */
+/* Per-pixel f32 mean (variance = 0) or variance_of_mean (variance = 1) of an
+ * accumulator, top-down RGB, computed on the GPU; on_device says whether the
+ * framebuffer pointers are device pointers. */
+int tv_image_pfm_pixels(const double* sum, const double* sum_sq, const uint32_t* counts, int32_t width, int32_t height,
+                        int32_t variance, int32_t on_device, int device, float* out_rgb);
+/* write_pfm / write_variance_pfm: byte-identical files */
+int tv_image_write_pfm(const char* path, const tv_framebuffer* fb, int32_t width, int32_t height, int32_t variance,
+                       int32_t on_device, int device);
+int tv_pfm_write(const char* path, const float* rgb, int32_t width, int32_t height);
+/* read_pfm: call with rgb = NULL for the size, then with 3*W*H floats */
+int tv_pfm_read(const char* path, int32_t* width, int32_t* height, float* rgb);
+/* a, b (and optional va, vb): 3 * n_pixels floats each (host) */
+int tv_image_compare(const float* a, const float* b, const float* va, const float* vb, uint64_t n_pixels, int device,
+                     tv_compare_stats* out);
 
 /* -- parity entry points ------------------------------------------------------ */
 /* Segments of n rays. offsets has n+1 entries; at most cap segments are

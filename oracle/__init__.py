@@ -196,6 +196,12 @@ class Checker:
             f("grid_load", _P, C.c_char_p)
             f("grid_save", C.c_int, _P, C.c_char_p)
             f("grid_set_payload", None, _P, C.c_uint32, C.c_float, C.c_float, C.c_float, C.c_uint32)
+            f("dvol_save", C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_char_p),
+              C.POINTER(_F))
+            f("dvol_load", C.c_int, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_char_p),
+              C.POINTER(_F))
+            f("write_pfm", C.c_int, C.c_char_p, C.c_int, C.c_int, _D, _D, _U32, C.c_int)
+            f("read_pfm", C.c_int, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _F)
             f("trace_sample", None, _P, C.POINTER(Camera), C.POINTER(RenderCfg), C.c_int, C.c_int, C.c_int, _D, _U64)
 
     def fn(self, name):

@@ -15,6 +15,8 @@
 //                                            include/tetvol/tracer.hpp:39-85
 //   PinholeCamera                             include/tetvol/camera.hpp:16-48
 //   RegularGrid::from_volume / render_reference include/tetvol/regular_grid.hpp:17-67
+//   DenseVolume save_dvol / load_dvol         include/tetvol/volume.hpp:19-58
+//   write_pfm / write_variance_pfm / read_pfm include/tetvol/image.hpp:72-90
 
 #include <cstdint>
 #include <cstring>
@@ -222,6 +224,70 @@ void ref_grid_export(void* h, uint32_t* vq, void* tets, uint32_t* roots) {
     if (tets) std::memcpy(tets, g->tets().data(), g->tet_count() * sizeof(Tet));
     if (roots)
         for (int i = 0; i < 24; ++i) roots[i] = g->roots()[i];
+}
+
+// DenseVolume(nx, ny, nz) + channels (names[0] must be "density"), save_dvol
+int ref_dvol_save(const char* path, int nx, int ny, int nz, int n_ch, const char* const* names,
+                  const float* const* data) {
+    try {
+        DenseVolume v(nx, ny, nz);
+        for (int c = 0; c < n_ch; ++c) {
+            std::vector<float>& d = c == 0 ? v.channel(names[0]) : v.add_channel(names[c]);
+            std::memcpy(d.data(), data[c], d.size() * sizeof(float));
+        }
+        v.save_dvol(path);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// load_dvol; out dims[3], n_ch; with data != NULL also copies the channels
+// (names: n_ch buffers of 256 bytes, data: n_ch arrays of nx*ny*nz floats)
+int ref_dvol_load(const char* path, int* dims, int* n_ch, char** names, float** data) {
+    try {
+        DenseVolume v = DenseVolume::load_dvol(path);
+        dims[0] = v.nx(), dims[1] = v.ny(), dims[2] = v.nz();
+        *n_ch = static_cast<int>(v.channel_names().size());
+        if (names && data)
+            for (int c = 0; c < *n_ch; ++c) {
+                const std::string& n = v.channel_names()[c];
+                std::strncpy(names[c], n.c_str(), 255);
+                names[c][255] = 0;
+                const auto& d = v.channel(n);
+                std::memcpy(data[c], d.data(), d.size() * sizeof(float));
+            }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_write_pfm(const char* path, int w, int h, const double* sum, const double* sum_sq, const uint32_t* counts,
+                  int variance) {
+    try {
+        ImageAccumulator img(w, h);
+        std::memcpy(img.sum.data(), sum, img.sum.size() * sizeof(double));
+        std::memcpy(img.sum_sq.data(), sum_sq, img.sum_sq.size() * sizeof(double));
+        std::memcpy(img.sample_counts.data(), counts, img.sample_counts.size() * sizeof(uint32_t));
+        if (variance) write_variance_pfm(path, img);
+        else write_pfm(path, img);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// read_pfm; rgb (3*w*h floats, top-down) may be NULL to query the size
+int ref_read_pfm(const char* path, int* w, int* h, float* rgb) {
+    try {
+        FloatImage img = read_pfm(path);
+        *w = img.width, *h = img.height;
+        if (rgb) std::memcpy(rgb, img.rgb.data(), img.rgb.size() * sizeof(float));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
 }
 
 // returns 1 when valid; out: leaf_count, interior_faces, boundary_faces

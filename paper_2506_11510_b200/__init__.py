@@ -64,8 +64,17 @@ class IoError(TetvolError):
     """errors.hpp: a file cannot be opened or written"""
 
 
+class VolumeError(TetvolError):
+    """volume.hpp:13-18 (and UnknownChannel)"""
+
+
+class ImageError(TetvolError):
+    """image.hpp: PFM I/O"""
+
+
 _ERRS = {1: TetvolError, 2: ConfigError, 3: CameraError, 4: GridError, 5: OutsideGrid, 6: CudaError,
-         7: CudaError, 8: ValueError, 9: FormatError, 10: IoError}
+         7: CudaError, 8: ValueError, 9: FormatError, 10: IoError, 11: VolumeError,
+         12: ImageError}
 
 
 def _check(rc: int):
@@ -523,8 +532,14 @@ def load_grid(path, device: int = 0) -> TetGrid:
     return TetGrid.load(path, device)
 
 
+from .image import (FloatImage, compare_images, pfm_pixels, read_pfm, render_accumulate,  # noqa: E402
+                    write_pfm, write_variance_pfm)
+from .volume import DenseVolume, build_adaptive_grid_volume  # noqa: E402
+
 __all__ = [
-    "BuildConfig", "BuildStats", "CameraError", "ConfigError", "CudaError", "FormatError", "GridError",
+    "BuildConfig", "BuildStats", "CameraError", "ConfigError", "CudaError", "DenseVolume", "FloatImage",
+    "FormatError", "GridError", "ImageError", "VolumeError", "build_adaptive_grid_volume", "compare_images",
+    "pfm_pixels", "read_pfm", "render_accumulate", "write_pfm", "write_variance_pfm",
     "ImageAccumulator", "IoError", "load_grid", "save_grid",
     "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
     "build_adaptive_grid", "build_adaptive_grid_dev", "device_count", "generate_volume_dev", "locate_points",

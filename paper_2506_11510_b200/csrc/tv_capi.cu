@@ -200,8 +200,11 @@ int workspace(int device, Workspace*& out) {
 
 // Renders this rank's tiles of one frame: per batch of samples, start ->
 // trace -> accumulate (see tv_trace.cu). Asynchronous on `st`.
+// Renders samples [first_sample, first_sample + spp) of this rank's pixels and
+// adds them to `out` in sample order (first_sample == 0 initialises it), so
+// frames that cover [0, N) leave exactly the framebuffer of one N-spp render.
 int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp, int rank, int n_ranks,
-                 RenderOut out, Workspace& w, cudaStream_t st) {
+                 RenderOut out, Workspace& w, cudaStream_t st, uint32_t first_sample = 0) {
     const uint32_t tiles_x = (static_cast<uint32_t>(cv.w) + 15) / 16;
     const uint32_t tiles_y = (static_cast<uint32_t>(cv.h) + 15) / 16;
     const uint64_t tiles = static_cast<uint64_t>(tiles_x) * tiles_y;
@@ -230,13 +233,13 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         w.n_launches += 3;
         Batch B;
         B.n_units = static_cast<uint32_t>(units);
-        B.s0 = static_cast<uint32_t>(s0);
+        B.s0 = first_sample + static_cast<uint32_t>(s0);
         B.ns = static_cast<uint32_t>(std::min<uint64_t>(ns, rp.spp - s0));
         B.tiles_x = tiles_x;
         B.rank = rank;
         B.n_ranks = n_ranks;
         B.n_paths = static_cast<uint32_t>(units * 32 * B.ns);
-        B.first = s0 == 0 ? 1u : 0u;
+        B.first = s0 == 0 && first_sample == 0 ? 1u : 0u;
         B.regen_min = w.regen_min;
         B.scatter_min = w.scatter_min;
         B.order = w.order;
@@ -462,6 +465,27 @@ int tv_render_tiles(const tv_grid* h, const tv_camera* camera, const tv_render_c
     std::lock_guard<std::mutex> lk(w->mu);
     RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
     return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream));
+}
+
+int tv_render_accumulate(const tv_grid* h, const tv_camera* camera, const tv_render_config* cfg,
+                         int32_t first_sample, int32_t rank, int32_t n_ranks, double* sum_dev, double* sum_sq_dev,
+                         uint32_t* counts_dev, uint64_t* stats_dev, void* stream) {
+    if (!h) return set_error(TV_ERR_ARG, "grid is null");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return set_error(TV_ERR_ARG, "bad rank / n_ranks");
+    if (first_sample < 0) return set_error(TV_ERR_ARG, "first_sample must be >= 0");
+    int rc = validate_render(cfg);
+    if (rc) return rc;
+    if (static_cast<int64_t>(first_sample) + cfg->spp > 0xffffffffll) return set_error(TV_ERR_ARG, "sample index overflow");
+    CamView cv;
+    if ((rc = host_camera(camera, cv, nullptr, nullptr))) return rc;
+    const DeviceGrid& g = h->g;
+    if ((rc = use_device(g.device))) return rc;
+    Workspace* w;
+    if ((rc = workspace(g.device, w))) return rc;
+    std::lock_guard<std::mutex> lk(w->mu);
+    RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
+    return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream),
+                        static_cast<uint32_t>(first_sample));
 }
 
 int tv_last_frame_timing(int device, double out[4]) {

@@ -97,6 +97,7 @@ __global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, Sta
 __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ cells, const double* __restrict__ rad,
                              RenderOut O) {
     const uint32_t n_px = B.n_units * 32u;
+    unsigned long long traced = 0;  // stats[1]: paths_traced (image.hpp:25)
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n_px; q += gridDim.x * blockDim.x) {
         const uint32_t unit = q >> 5, lane = q & 31u;
         const uint32_t p0 = path_id(B, unit, lane, 0);
@@ -104,6 +105,7 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
         uint32_t s;
         path_pixel(B, p0, px, py, s);
         if (px >= C.w || py >= C.h) continue;
+        traced += B.ns;
         const uint64_t pix = static_cast<uint64_t>(py) * static_cast<uint64_t>(C.w) + px;
         double sr = 0.0, sg = 0.0, sb = 0.0, qr = 0.0, qg = 0.0, qb = 0.0;
         uint32_t n = 0;
@@ -122,6 +124,10 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
         if (O.sum) O.sum[3 * pix] = sr, O.sum[3 * pix + 1] = sg, O.sum[3 * pix + 2] = sb;
         if (O.sum_sq) O.sum_sq[3 * pix] = qr, O.sum_sq[3 * pix + 1] = qg, O.sum_sq[3 * pix + 2] = qb;
         if (O.counts) O.counts[pix] = n;
+    }
+    if (O.stats) {
+        for (int o = 16; o; o >>= 1) traced += __shfl_down_sync(kFull, traced, o);
+        if ((threadIdx.x & 31) == 0 && traced) atomicAdd(reinterpret_cast<unsigned long long*>(O.stats + 1), traced);
     }
 }
 

@@ -296,3 +296,41 @@ def test_tgrid_restatement_matches_reference(tmp_path):
         assert ref.fn("grid_save")(g.h, fn.encode()) == 0
         p = g.pools()
         assert tgrid_bytes(p.vq, p.tets, p.roots) == open(fn, "rb").read()
+
+
+@needs_ref
+def test_pfm_restatement_matches_reference(tmp_path):
+    from oracle.images import mean_f32, pfm_bytes, variance_f32
+
+    rng = np.random.default_rng(4)
+    w, h = 7, 5
+    cnt = rng.integers(0, 4, w * h).astype(np.uint32)
+    s = rng.random(3 * w * h) * cnt.repeat(3)
+    q = s * s / np.maximum(cnt, 1).repeat(3) + rng.random(3 * w * h) * 0.1
+    for variance in (0, 1):
+        fn = str(tmp_path / f"r{variance}.pfm")
+        assert ref.fn("write_pfm")(fn.encode(), w, h, s.ctypes.data_as(_D), q.ctypes.data_as(_D),
+                                   cnt.ctypes.data_as(C.POINTER(C.c_uint32)), variance) == 0
+        px = variance_f32(s, q, cnt) if variance else mean_f32(s, cnt)
+        raw = open(fn, "rb").read()
+        assert pfm_bytes(px, w, h) == raw
+        W, H = C.c_int(), C.c_int()
+        back = np.zeros(3 * w * h, np.float32)
+        assert ref.fn("read_pfm")(fn.encode(), C.byref(W), C.byref(H), back.ctypes.data_as(C.POINTER(C.c_float))) == 0
+        assert (W.value, H.value) == (w, h) and np.array_equal(back, px.ravel())
+
+
+@needs_ref
+def test_dvol_restatement_matches_reference(tmp_path):
+    from oracle.images import dvol_bytes
+
+    dims = (5, 4, 3)
+    rng = np.random.default_rng(2)
+    chans = {"density": rng.random((3, 4, 5), dtype=np.float32), "temperature": rng.random((3, 4, 5), dtype=np.float32),
+             "albedo": np.full((3, 4, 5), 0.25, np.float32)}
+    fn = str(tmp_path / "v.dvol")
+    names = (C.c_char_p * 3)(*[k.encode() for k in chans])
+    F = C.POINTER(C.c_float)
+    data = (F * 3)(*[v.ctypes.data_as(F) for v in chans.values()])
+    assert ref.fn("dvol_save")(fn.encode(), *dims, 3, names, data) == 0
+    assert dvol_bytes(dims, chans) == open(fn, "rb").read()
