@@ -284,6 +284,25 @@ int tv_pfm_read(const char* path, int32_t* width, int32_t* height, float* rgb);
 int tv_image_compare(const float* a, const float* b, const float* va, const float* vb, uint64_t n_pixels, int device,
                      tv_compare_stats* out);
 
+/* -- validation (TetGrid::validate, tet_grid.cpp:474-636) --------------------- */
+typedef struct {
+    int32_t ok;
+    int32_t pad;
+    uint64_t leaf_count;
+    uint64_t interior_faces;
+    uint64_t boundary_faces;
+    char first_violation[128];
+} tv_validation_report;
+/* The reference's exhaustive invariant checks on the GPU, over the grid's
+ * reference-layout pools; first_violation is the reference's first message. */
+int tv_grid_validate(const tv_grid* g, tv_validation_report* out);
+/* cmd_validate's traversal spot checks (cli.cpp:565-595): for each ray, our
+ * march_segments against the brute-force traverser (tet_grid.cpp:659-698, on
+ * the GPU), segments <= 1e-12 dropped; same cells and lengths within 1e-9. */
+int tv_validate_rays(const tv_grid* g, const tv_ray* rays, int32_t n, int32_t* failures, int32_t* first_failed);
+/* cmd_validate's n spot-check rays for a seed (cli.cpp:552-569), on the host */
+int tv_validate_spot_rays(uint64_t seed, int32_t n, tv_ray* out);
+
 /* -- parity entry points ------------------------------------------------------ */
 /* Segments of n rays. offsets has n+1 entries; at most cap segments are
  * written; *total receives the full count. */

@@ -18,6 +18,8 @@
 //   DenseVolume save_dvol / load_dvol         include/tetvol/volume.hpp:19-58
 //   write_pfm / write_variance_pfm / read_pfm include/tetvol/image.hpp:72-90
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -366,6 +368,55 @@ int64_t ref_march_segments(void* h, const double* rays, uint64_t n, uint32_t* ce
         stats[1] = st.degenerate_paths;
     }
     return static_cast<int64_t>(k);
+}
+
+// cmd_validate's spot-check rays (cli.cpp:552-569; sphere_dir is file-local
+// there, restated here): origin on the radius-2 sphere, target in the middle half
+void ref_spot_rays(uint64_t seed, int n, double* out) {
+    const Vec3 center{0.5, 0.5, 0.5};
+    for (int i = 0; i < n; ++i) {
+        RngStream rng(seed, 0x76616c6964617465ull, static_cast<std::uint64_t>(i));
+        const double u1 = rng.next(), u2 = rng.next();
+        const double z = 1.0 - 2.0 * u1;
+        const double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+        const double phi = 2.0 * 3.14159265358979323846 * u2;
+        const Vec3 origin = center + Vec3{r * std::cos(phi), r * std::sin(phi), z} * 2.0;
+        const double tx = 0.25 + 0.5 * rng.next(), ty = 0.25 + 0.5 * rng.next(), tz = 0.25 + 0.5 * rng.next();
+        const Ray ray{origin, normalize(Vec3{tx, ty, tz} - origin)};
+        double* o = out + 8 * i;
+        o[0] = ray.origin.x, o[1] = ray.origin.y, o[2] = ray.origin.z;
+        o[3] = ray.dir.x, o[4] = ray.dir.y, o[5] = ray.dir.z, o[6] = ray.t_min, o[7] = ray.t_max;
+    }
+}
+
+// the spot-check loop itself (cli.cpp:569-595) with the reference's
+// march_segments and BruteForceTraverser
+void ref_spot_checks(void* h, int n, uint64_t seed, int* failures, int* first) {
+    const TetGrid& grid = *static_cast<TetGrid*>(h);
+    BruteForceTraverser oracle(grid);
+    std::vector<double> rays(8 * static_cast<size_t>(n));
+    ref_spot_rays(seed, n, rays.data());
+    *failures = 0, *first = -1;
+    auto keep = [](const std::vector<RaySegment>& in) {
+        std::vector<RaySegment> o;
+        for (const auto& s : in)
+            if (s.t_exit - s.t_enter > 1e-12) o.push_back(s);
+        return o;
+    };
+    for (int i = 0; i < n; ++i) {
+        const double* r = &rays[8 * static_cast<size_t>(i)];
+        Ray ray{v3(r), v3(r + 3), r[6], r[7]};
+        auto got = keep(march_segments(grid, ray));
+        auto want = keep(oracle.segments(ray));
+        bool ok = got.size() == want.size();
+        for (std::size_t k = 0; ok && k < got.size(); ++k)
+            ok = got[k].cell == want[k].cell &&
+                 std::fabs((got[k].t_exit - got[k].t_enter) - (want[k].t_exit - want[k].t_enter)) <= 1e-9;
+        if (!ok) {
+            ++*failures;
+            if (*first < 0) *first = i;
+        }
+    }
 }
 
 double ref_march_transmittance(void* h, const double* r) {

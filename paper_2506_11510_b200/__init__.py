@@ -117,6 +117,11 @@ class _Framebuffer(C.Structure):
                 ("sample_counts", C.POINTER(C.c_uint32))]
 
 
+class _ValidationReport(C.Structure):
+    _fields_ = [("ok", C.c_int32), ("pad", C.c_int32), ("leaf_count", C.c_uint64), ("interior_faces", C.c_uint64),
+                ("boundary_faces", C.c_uint64), ("first_violation", C.c_char * 128)]
+
+
 class _GridInfo(C.Structure):
     _fields_ = [("n_vertices", C.c_uint64), ("n_tets", C.c_uint64), ("n_leaves", C.c_uint64),
                 ("n_internal", C.c_uint64), ("max_level", C.c_int32), ("max_depth", C.c_int32),
@@ -145,6 +150,9 @@ _sig("tv_grid_download", C.c_int, _P, _P, _P, _U32)
 _sig("tv_grid_get_info", C.c_int, _P, C.POINTER(_GridInfo))
 _sig("tv_grid_free", None, _P)
 _sig("tv_grid_save", C.c_int, _P, C.c_char_p)
+_sig("tv_grid_validate", C.c_int, _P, _P)
+_sig("tv_validate_rays", C.c_int, _P, _P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32))
+_sig("tv_validate_spot_rays", C.c_int, C.c_uint64, C.c_int32, _P)
 _sig("tv_grid_load", C.c_int, C.c_char_p, C.c_int, C.POINTER(_P))
 _sig("tv_build", C.c_int, _F, _F, _F, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_BuildConfig), C.POINTER(_Camera),
      C.c_int, C.POINTER(_P), C.POINTER(_BuildStats))
@@ -336,6 +344,20 @@ class TetGrid:
         _check(_lib.tv_grid_download(self.handle, v.ctypes.data_as(_P), t.ctypes.data_as(_P), r.ctypes.data_as(_U32)))
         return v, t, r
 
+    def validate(self) -> dict:
+        """TetGrid::validate (tet_grid.cpp:474-636) on the GPU: the reference's report fields."""
+        r = _ValidationReport()
+        _check(_lib.tv_grid_validate(self.handle, C.byref(r)))
+        return dict(ok=bool(r.ok), firstViolation=r.first_violation.decode() or None, leafCount=r.leaf_count,
+                    interiorFaces=r.interior_faces, boundaryFaces=r.boundary_faces)
+
+    def spot_check(self, rays: int = 100, seed: int = 0) -> tuple:
+        """cmd_validate's traversal spot checks (cli.cpp:565-595) -> (failures, first failing ray or -1)."""
+        r = spot_rays(seed, rays)
+        f, first = C.c_int32(), C.c_int32()
+        _check(_lib.tv_validate_rays(self.handle, r.ctypes.data_as(_P), len(r), C.byref(f), C.byref(first)))
+        return f.value, first.value
+
     def save(self, path) -> None:
         """save_grid (builder.hpp:59): the reference's TGRD v1 file, packed on the device."""
         _check(_lib.tv_grid_save(self.handle, os.fsencode(path)))
@@ -522,6 +544,13 @@ def render_reference_dev(density_dev: int, shape, density_scale: float, camera: 
     return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
 
 
+def spot_rays(seed: int, n: int) -> np.ndarray:
+    """cmd_validate's spot-check rays (cli.cpp:552-569), (n, 8) float64 [origin, dir, t_min, t_max]."""
+    out = np.zeros((n, 8), np.float64)
+    _check(_lib.tv_validate_spot_rays(int(seed), int(n), out.ctypes.data_as(_P)))
+    return out
+
+
 def save_grid(grid: TetGrid, path) -> None:
     """builder.hpp:59"""
     grid.save(path)
@@ -540,7 +569,7 @@ __all__ = [
     "BuildConfig", "BuildStats", "CameraError", "ConfigError", "CudaError", "DenseVolume", "FloatImage",
     "FormatError", "GridError", "ImageError", "VolumeError", "build_adaptive_grid_volume", "compare_images",
     "pfm_pixels", "read_pfm", "render_accumulate", "write_pfm", "write_variance_pfm",
-    "ImageAccumulator", "IoError", "load_grid", "save_grid",
+    "ImageAccumulator", "IoError", "load_grid", "save_grid", "spot_rays",
     "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
     "build_adaptive_grid", "build_adaptive_grid_dev", "device_count", "generate_volume_dev", "locate_points",
     "march_segments", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",

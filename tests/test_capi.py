@@ -120,3 +120,20 @@ def test_tgrid_header_errors_before_device(tmp_path):
         fn.write_bytes(tgrid_bytes(p.vq, p.tets, p.roots))
         with pytest.raises(tv.CudaError):
             tv.load_grid(fn)
+
+
+def test_spot_rays_match_reference_cli():
+    """cmd_validate's spot-check rays are generated on the host: bit-identical to cli.cpp:552-569."""
+    import ctypes as C
+
+    import oracle as O
+    import paper_2506_11510_b200 as tv
+
+    ref = O.ref_oracle()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    for seed in (0, 7, 2**63 + 5):
+        mine = tv.spot_rays(seed, 300)
+        want = np.zeros((300, 8))
+        ref.fn("spot_rays")(seed, 300, want.ctypes.data_as(C.POINTER(C.c_double)))
+        assert np.array_equal(mine.view(np.uint64), want.view(np.uint64))
