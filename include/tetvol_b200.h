@@ -185,6 +185,13 @@ const char* tv_last_error(void);
 const char* tv_version(void);
 int tv_device_count(int* out);
 
+/* Validation alone, no device work: the PinholeCamera constructor
+ * (camera.cpp:12-20), RenderConfig::validate (tracer.cpp:131-141) and
+ * BuildConfig::validate (builder.cpp:12-17), with their messages. */
+int tv_check_camera(const tv_camera* camera);
+int tv_check_render_config(const tv_render_config* cfg);
+int tv_check_build_config(const tv_build_config* cfg);
+
 /* -- grid lifetime -------------------------------------------------------- */
 int tv_grid_upload(const tv_vertex* vertices, uint64_t n_vertices, const tv_tet* tets, uint64_t n_tets,
                    const uint32_t roots[24], int32_t max_level, int device, tv_grid** out);

@@ -1261,6 +1261,8 @@ int prevalidate(const tv_build_config* cfg, const tv_camera* camera) {
 
 extern "C" {
 
+int tv_check_build_config(const tv_build_config* cfg) { return validate_build_cfg(cfg); }
+
 int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, double value, float* out_dev,
                            int device) {
     if (!out_dev) return set_error(TV_ERR_ARG, "null output");

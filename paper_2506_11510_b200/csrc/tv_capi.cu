@@ -488,6 +488,13 @@ int tv_render_accumulate(const tv_grid* h, const tv_camera* camera, const tv_ren
                         static_cast<uint32_t>(first_sample));
 }
 
+int tv_check_camera(const tv_camera* camera) {
+    CamView cv;
+    return host_camera(camera, cv, nullptr, nullptr);
+}
+
+int tv_check_render_config(const tv_render_config* cfg) { return validate_render(cfg); }
+
 int tv_last_frame_timing(int device, double out[4]) {
     if (!out) return set_error(TV_ERR_ARG, "out is null");
     int rc = use_device(device);
