@@ -26,6 +26,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -783,10 +785,14 @@ __global__ void gather_face_hi_kernel(const uint32_t* rec, uint64_t n, const uin
 // ------------------------------------------------------------ host side
 inline unsigned nblk(uint64_t n, unsigned t = 256) { return static_cast<unsigned>(std::max<uint64_t>((n + t - 1) / t, 1)); }
 
+// Build scratch comes from the device's stream-ordered memory pool (kept
+// cached across builds, see build_grid), not from cudaMalloc / cudaFree.
 struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
-    ~Buf() { cudaFree(p); }
+    ~Buf() {
+        if (p) cudaFreeAsync(p, 0);
+    }
     template <class T>
     T* as() {
         return static_cast<T*>(p);
@@ -796,17 +802,28 @@ struct Buf {
 int ensure(Buf& b, size_t bytes, bool keep = false) {
     if (b.bytes >= bytes) return TV_OK;
     size_t nb = std::max(bytes, b.bytes + b.bytes / 2);
+    struct Timer {
+        size_t nb;
+        std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+        ~Timer() {
+            static const bool v = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
+            if (!v || nb < (256u << 20)) return;
+            cudaDeviceSynchronize();
+            std::fprintf(stderr, "tetvol_b200: build alloc %.1f MB %.2f ms\n", nb / 1048576.0,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        }
+    } timer{nb};
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, nb);
+    cudaError_t e = cudaMallocAsync(&p, nb, 0);
     if (e != cudaSuccess) return cuda_status(e, "build alloc");
     if (keep && b.p && b.bytes) {
-        e = cudaMemcpy(p, b.p, b.bytes, cudaMemcpyDeviceToDevice);
+        e = cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, 0);
         if (e != cudaSuccess) {
-            cudaFree(p);
+            cudaFreeAsync(p, 0);
             return cuda_status(e, "build grow");
         }
     }
-    cudaFree(b.p);
+    if (b.p) cudaFreeAsync(b.p, 0);
     b.p = p;
     b.bytes = nb;
     return TV_OK;
@@ -875,6 +892,13 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     if (rc) return rc;
     if (cfg->use_camera && !camera) return set_error(TV_ERR_CONFIG, "useCamera set but no camera given");
     if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR_CONFIG, "volume dimensions must be positive");
+    {  // keep up to 16 GB of build scratch cached in the pool between builds
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = 16ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     EvalParams E{};
     E.thr = cfg->variation_threshold;
     E.max_level = cfg->max_level;
@@ -1010,8 +1034,15 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     TRY(ensure(fresh_b, 24 * sizeof(uint32_t)));
     CK(cudaMemcpy(fresh_b.p, roots, sizeof(roots), cudaMemcpyHostToDevice), "fresh");
     int herr = 0;
+    const bool verbose = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto since = [&](std::chrono::steady_clock::time_point t) {
+        cudaDeviceSynchronize();
+        return std::chrono::duration<double, std::milli>(now() - t).count();
+    };
 
     for (;;) {
+        const auto t_round = now();
         // ---- eval fresh leaves ----
         if (rounds > 0) {
             owner_descend_kernel<<<148 * 8, 256>>>(split_b.as<NodeRec>(), tets_b.as<tv_tet>(), nx, ny, nz,
@@ -1027,11 +1058,20 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
                                                   flags_b.as<uint8_t>(), d_ctr);
         CK(cudaGetLastError(), "eval");
         TRY(select_flagged(fresh_b.as<uint32_t>(), n_fresh, F_MARK, marked_b, n_marked, false));
+        const double ms_eval = verbose ? since(t_round) : 0.0;
+        if (verbose) {
+            unsigned long long c[2];
+            cudaMemcpy(c, d_ctr, sizeof(c), cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "tetvol_b200: build round %d: fresh %u marked %u eval %.2f ms (replays %llu)\n",
+                         rounds, n_fresh, n_marked, ms_eval, c[0]);
+        }
         if (n_marked == 0) break;
         crit += n_marked;
         ++rounds;
         // ---- closure ----
+        double ph[4] = {0, 0, 0, 0};  // verbose: midpoint+dedup, bisect, leaves+hanging, select
         while (n_marked) {
+            auto tp = now();
             TRY(grow_tets(static_cast<size_t>(n_t) + 2ull * n_marked));
             TRY(grow_verts(static_cast<size_t>(n_v) + n_marked));
             TRY(ensure(mid_b, n_marked * sizeof(uint32_t)));
@@ -1099,6 +1139,7 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
                 CK(cudaGetLastError(), "dedup assign");
                 n_v += n_new;
             }
+            if (verbose) ph[0] += since(tp), tp = now();
             CK(cudaMemset(vtouch_b.p, 0, n_v), "vtouch");
             bisect_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, n_t, tets_b.as<tv_tet>(),
                                                    verts_b.as<uint4>(), mid_b.as<uint32_t>(), split_b.as<NodeRec>(),
@@ -1109,6 +1150,7 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
             ++passes;
             CK(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost), "err");
             if (herr) break;
+            if (verbose) ph[1] += since(tp), tp = now();
             // leaf list, hanging test
             TRY(select_flagged(nullptr, n_t, F_LEAF, leaves_b, n_leaves, true));
             CK(cudaMemset(d_cnt, 0, sizeof(uint32_t)), "memset");
@@ -1116,13 +1158,20 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
                                                     verts_b.as<uint4>(), table_b.as<uint32_t>(), hmask,
                                                     vtouch_b.as<uint8_t>(), flags_b.as<uint8_t>(), d_cnt);
             CK(cudaGetLastError(), "hanging");
+            if (verbose) ph[2] += since(tp), tp = now();
             TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_MARK, marked_b, n_marked, false));
             clear_flag_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, flags_b.as<uint8_t>(), F_MARK);
             CK(cudaGetLastError(), "clear");
+            if (verbose) ph[3] += since(tp);
         }
+        if (verbose)
+            std::fprintf(stderr, "tetvol_b200: build round %d phases: mid+dedup %.1f bisect %.1f hanging %.1f select %.1f ms\n",
+                         rounds, ph[0], ph[1], ph[2], ph[3]);
         if (herr) break;
         // fresh = leaves created in this round
         TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_NEW, fresh_b, n_fresh, false));
+        if (verbose) std::fprintf(stderr, "tetvol_b200: build round %d: closure done, %.2f ms total\n", rounds,
+                                  since(t_round));
     }
     if (herr) {
         if (herr & E_LEVEL) return set_error(TV_ERR_GRID, "bisect: level cap reached");

@@ -95,8 +95,17 @@ def c4():
             break
 
 
+def warmup():
+    """one small build + render first, so no row pays the process's first-use costs"""
+    vol = field(64)
+    g, _ = build(vol, 64, 0.15, 18)
+    render(g, spp=1, frames=1)
+    g.close()
+
+
 if __name__ == "__main__":
     rows = sys.argv[1:] or ["c2", "c3", "c4"]
+    warmup()
     if "c2" in rows:
         c2()
     if "c3" in rows or "c5" in rows:
