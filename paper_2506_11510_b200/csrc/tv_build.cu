@@ -801,21 +801,22 @@ struct Buf {
 
 int ensure(Buf& b, size_t bytes, bool keep = false) {
     if (b.bytes >= bytes) return TV_OK;
-    size_t nb = std::max(bytes, b.bytes + b.bytes / 2);
-    struct Timer {
-        size_t nb;
-        std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-        ~Timer() {
-            static const bool v = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
-            if (!v || nb < (256u << 20)) return;
-            cudaDeviceSynchronize();
-            std::fprintf(stderr, "tetvol_b200: build alloc %.1f MB %.2f ms\n", nb / 1048576.0,
-                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-        }
-    } timer{nb};
+    const size_t nb = std::max(bytes, 2 * b.bytes);  // doubling: each pool growth maps GBs (10-300 ms)
+    static const bool verbose = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
+    const bool log = verbose && nb >= (256u << 20);
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&]() {
+        cudaDeviceSynchronize();
+        const auto t = std::chrono::steady_clock::now();
+        const double ms = std::chrono::duration<double, std::milli>(t - t0).count();
+        t0 = t;
+        return ms;
+    };
+    if (log) lap();
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, nb, 0);
     if (e != cudaSuccess) return cuda_status(e, "build alloc");
+    const double ms_alloc = log ? lap() : 0.0;
     if (keep && b.p && b.bytes) {
         e = cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, 0);
         if (e != cudaSuccess) {
@@ -823,7 +824,12 @@ int ensure(Buf& b, size_t bytes, bool keep = false) {
             return cuda_status(e, "build grow");
         }
     }
+    const double ms_copy = log ? lap() : 0.0;
     if (b.p) cudaFreeAsync(b.p, 0);
+    const double ms_free = log ? lap() : 0.0;
+    if (log)
+        std::fprintf(stderr, "tetvol_b200: build alloc %.1f MB: malloc %.2f copy %.2f free %.2f ms\n", nb / 1048576.0,
+                     ms_alloc, ms_copy, ms_free);
     b.p = p;
     b.bytes = nb;
     return TV_OK;
@@ -892,10 +898,10 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     if (rc) return rc;
     if (cfg->use_camera && !camera) return set_error(TV_ERR_CONFIG, "useCamera set but no camera given");
     if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR_CONFIG, "volume dimensions must be positive");
-    {  // keep up to 16 GB of build scratch cached in the pool between builds
+    {  // keep up to 32 GB of build scratch cached in the pool between builds
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t keep = 16ull << 30;
+            uint64_t keep = 32ull << 30;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     }
@@ -1041,6 +1047,19 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
         return std::chrono::duration<double, std::milli>(now() - t).count();
     };
 
+    // TV_VERBOSE=3: per-round GPU time (events, no host syncs) next to host time
+    const bool evlog = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) == 3;
+    std::vector<cudaEvent_t> marks;
+    std::vector<double> host_ms;
+    auto mark = [&]() {
+        if (!evlog) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, 0);
+        marks.push_back(e);
+        host_ms.push_back(std::chrono::duration<double, std::milli>(now().time_since_epoch()).count());
+    };
+    mark();
     for (;;) {
         const auto t_round = now();
         // ---- eval fresh leaves ----
@@ -1172,6 +1191,7 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
         TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_NEW, fresh_b, n_fresh, false));
         if (verbose) std::fprintf(stderr, "tetvol_b200: build round %d: closure done, %.2f ms total\n", rounds,
                                   since(t_round));
+        mark();
     }
     if (herr) {
         if (herr & E_LEVEL) return set_error(TV_ERR_GRID, "bisect: level cap reached");
@@ -1232,6 +1252,16 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     }
     CK(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost), "err");
     if (herr & E_FACE) return set_error(TV_ERR_GRID, "face shared by more than two leaves");
+    if (evlog && marks.size() > 1) {
+        cudaDeviceSynchronize();
+        for (size_t k = 1; k < marks.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[k - 1], marks[k]);
+            std::fprintf(stderr, "tetvol_b200: build round %zu: gpu %.1f ms host %.1f ms\n", k, ms,
+                         host_ms[k] - host_ms[k - 1]);
+        }
+        for (auto e : marks) cudaEventDestroy(e);
+    }
     unsigned long long hctr[2] = {0, 0};
     CK(cudaMemcpy(hctr, d_ctr, sizeof(hctr), cudaMemcpyDeviceToHost), "counters");
     cudaEventRecord(e1);
