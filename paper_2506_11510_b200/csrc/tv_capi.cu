@@ -236,6 +236,7 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.s0 = first_sample + static_cast<uint32_t>(s0);
         B.ns = static_cast<uint32_t>(std::min<uint64_t>(ns, rp.spp - s0));
         B.tiles_x = tiles_x;
+        B.tiles_y = tiles_y;
         B.rank = rank;
         B.n_ranks = n_ranks;
         B.n_paths = static_cast<uint32_t>(units * 32 * B.ns);

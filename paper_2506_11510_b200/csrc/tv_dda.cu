@@ -242,6 +242,7 @@ static int render_regular(const float* density, bool on_device, int32_t nx, int3
         B.s0 = static_cast<uint32_t>(s0);
         B.ns = static_cast<uint32_t>(std::min<uint64_t>(ns, rp.spp - s0));
         B.tiles_x = tiles_x;
+        B.tiles_y = tiles_y;
         B.rank = 0;
         B.n_ranks = 1;
         B.n_paths = static_cast<uint32_t>(units * 32 * B.ns);

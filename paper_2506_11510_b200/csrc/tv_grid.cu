@@ -78,12 +78,13 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
         const uint32_t id = static_cast<uint32_t>(tt.normal_ids[f]) & 31u;
         r.w[f] = (nb == kNone ? kNoLeaf : tet2leaf[nb]) | (id << 27);
         // exit_face reads vertex verts[(f+1)&3] of face f (tracer.cpp:152)
-        const uint32_t code = face_code(tt.normal_ids[f]);
         const uint4 q = verts[tt.verts[(f + 1) & 3]];
         const uint32_t qq[3] = {q.x, q.y, q.z};
-        r.w[4 + 2 * f] = __float_as_uint(static_cast<float>(qq[code & 3u]) * 0x1.0p-24f);
-        r.w[5 + 2 * f] = __float_as_uint(static_cast<float>(qq[(code >> 2) & 3u]) * 0x1.0p-24f);
-        codes |= leaf_code6(face_code(id & ~1u)) << (6 * f);
+        uint32_t ai, aj;
+        pos2_axes(id, ai, aj);
+        r.w[4 + 2 * f] = __float_as_uint(static_cast<float>(qq[ai]) * 0x1.0p-24f);
+        r.w[5 + 2 * f] = __float_as_uint(static_cast<float>(qq[aj]) * 0x1.0p-24f);
+        codes |= pos2_code(id) << (6 * f);
     }
     r.w[12] = codes | (static_cast<uint32_t>(tt.mask & 7u) << 24);
     mask[L] = tt.mask;

@@ -22,7 +22,7 @@ constexpr uint64_t kMaxBatchPaths = 1ull << 26;
 struct Batch {
     uint32_t n_units;
     uint32_t s0, ns;
-    uint32_t tiles_x;
+    uint32_t tiles_x, tiles_y;
     int32_t rank, n_ranks;
     uint32_t n_paths;
     uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
