@@ -147,6 +147,7 @@ struct Workspace {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int trace_blocks = 0, sms = 0;
     TraceFn trace = nullptr;
+    int trace_threads = kTraceThreads;
     uint32_t regen_min = 8, scatter_min = 8, order = 0;
     cudaEvent_t tev[4 * 8] = {};  // per-batch kernel boundaries of the last frame
     int n_timed = 0, n_launches = 0;
@@ -178,8 +179,9 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaEventCreate(&w.ev1), "event create");
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
         // tuning knobs (defaults are the measured best on B200)
+        const int slots = 1;
         const int maxreg = env_int("TV_TRACE_MAXREG", 128);
-        w.trace = trace_variant(maxreg);
+        w.trace = trace_variant(maxreg, slots, w.trace_threads);
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 1));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
@@ -187,11 +189,12 @@ int workspace(int device, Workspace*& out) {
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
                              env_int("TV_CARVEOUT", 50));
         cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace), kTraceThreads,
-                                                      0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace),
+                                                      w.trace_threads, 0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
         if (env_int("TV_VERBOSE", 0))
-            std::fprintf(stderr, "tetvol_b200: trace kernel maxreg=%d, %d blocks/SM resident, %d blocks\n", maxreg, per_sm,
+            std::fprintf(stderr, "tetvol_b200: trace kernel maxreg=%d slots=%d, %d blocks/SM resident, %d blocks\n", maxreg,
+                         slots, per_sm,
                          w.trace_blocks);
     }
     out = &w;
@@ -250,7 +253,7 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         TV_CK(cudaGetLastError(), "start_kernel launch");
         TV_CK(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), st), "memset counter");
         if (ev) TV_CK(cudaEventRecord(ev[1], st), "event");
-        w.trace<<<w.trace_blocks, kTraceThreads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
+        w.trace<<<w.trace_blocks, w.trace_threads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
                                                           w.counter);
         TV_CK(cudaGetLastError(), "trace_kernel launch");
         if (ev) TV_CK(cudaEventRecord(ev[2], st), "event");
