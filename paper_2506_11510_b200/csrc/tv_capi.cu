@@ -183,7 +183,7 @@ int workspace(int device, Workspace*& out) {
         const int maxreg = env_int("TV_TRACE_MAXREG", 128);
         w.trace = trace_variant(maxreg, slots, w.trace_threads);
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
-        w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 1));
+        w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 2));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
         int per_sm = 1;
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
