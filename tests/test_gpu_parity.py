@@ -209,3 +209,28 @@ def test_config_errors_mirror_reference(tv, c1):
         tv.render(dg, tv.PinholeCamera(vfov_degrees=180.0), tv.RenderConfig())
     with pytest.raises(tv.CameraError, match="parallel"):
         tv.render(dg, tv.PinholeCamera(forward=(0, 1, 0), up=(0, 1, 0)), tv.RenderConfig())
+
+
+def test_multi_batch_frame_matches_progressive_frames(tv, c1):
+    """A frame larger than one sample batch (2^26 paths) is rendered in several
+    batches; their ordered accumulation must equal rendering the same samples as
+    progressive single-batch frames (tv_render_accumulate), bit for bit."""
+    import torch
+
+    _, _, dg = c1
+    w, h, spp = 512, 512, 300  # 78.6M paths -> 2 batches of the trace kernel
+    cam = tv.PinholeCamera((0.5, 0.5, -2), (0, 0, 1), (0, 1, 0), 40, w, h)
+    rc = tv.RenderConfig(spp=spp, max_bounces=2, seed=3)
+    full = tv.render(dg, cam, rc)
+    s = torch.zeros(3 * w * h, dtype=torch.float64, device="cuda")
+    q = torch.zeros_like(s)
+    c = torch.zeros(w * h, dtype=torch.int32, device="cuda")
+    first = 0
+    for part in (100, 100, 100):
+        tv.render_accumulate(dg, cam, tv.RenderConfig(spp=part, max_bounces=2, seed=3), first, s.data_ptr(),
+                             q.data_ptr(), c.data_ptr(), None)
+        first += part
+    torch.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy().view(np.uint64), full.sum.view(np.uint64))
+    assert np.array_equal(q.cpu().numpy().view(np.uint64), full.sum_sq.view(np.uint64))
+    assert np.all(c.cpu().numpy() == spp) and full.paths_traced == w * h * spp
