@@ -315,6 +315,22 @@ int tv_validate_spot_rays(uint64_t seed, int32_t n, tv_ray* out);
  * written; *total receives the full count. */
 int tv_march_segments(const tv_grid* g, const tv_ray* rays, uint64_t n, tv_segment* out, uint64_t* offsets,
                       uint64_t cap, uint64_t* total, uint64_t* degenerate_paths);
+/* FreePathSample (tracer.hpp:54-60); cell is the reference TetId. */
+typedef struct {
+    int32_t collided;
+    uint32_t cell;
+    double distance;
+    double position[3];
+} tv_free_path;
+
+/* march_transmittance (tracer.hpp:52) per ray: tau_out = the optical depth
+ * (bit-exact), trans_out = exp(-tau); either may be NULL. stats (may be NULL):
+ * cells_visited, degenerate_paths. */
+int tv_march_transmittance(const tv_grid* g, const tv_ray* rays, uint64_t n, double* tau_out, double* trans_out,
+                           uint64_t stats[2]);
+/* sample_free_path (tracer.hpp:63) per ray with RngStream(seed, pixels[i], samples[i]). */
+int tv_sample_free_path(const tv_grid* g, const tv_ray* rays, uint64_t n, uint64_t seed, const uint64_t* pixels,
+                        const uint64_t* samples, tv_free_path* out, uint64_t stats[2]);
 /* points: 3*n doubles; out: reference TetIds (TV_NO_TET when outside). */
 int tv_locate_points(const tv_grid* g, const double* points, uint64_t n, uint32_t* out);
 

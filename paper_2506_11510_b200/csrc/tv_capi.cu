@@ -550,6 +550,62 @@ int tv_march_segments(const tv_grid* h, const tv_ray* rays, uint64_t n, tv_segme
     return TV_OK;
 }
 
+namespace {
+// shared driver of tv_march_transmittance / tv_sample_free_path
+int medium(const tv_grid* h, const tv_ray* rays, uint64_t n, int mode, uint64_t seed, const uint64_t* pixels,
+           const uint64_t* samples, double* tau_out, double* trans_out, tv_free_path* fp_out, uint64_t* stats) {
+    if (!h || (!rays && n) || (mode == 1 && n && (!pixels || !samples))) return set_error(TV_ERR_ARG, "null argument");
+    const DeviceGrid& g = h->g;
+    int rc = use_device(g.device);
+    if (rc) return rc;
+    struct Dev {
+        void* p = nullptr;
+        ~Dev() {
+            if (p) cudaFree(p);
+        }
+    } d_rays, d_pix, d_smp, d_tau, d_tr, d_fp, d_ctr;
+    const uint64_t m = n ? n : 1;
+    TV_CK(cudaMalloc(&d_rays.p, m * sizeof(tv_ray)), "alloc");
+    TV_CK(cudaMalloc(&d_ctr.p, 2 * sizeof(unsigned long long)), "alloc");
+    TV_CK(cudaMemset(d_ctr.p, 0, 2 * sizeof(unsigned long long)), "memset");
+    if (n) TV_CK(cudaMemcpy(d_rays.p, rays, n * sizeof(tv_ray), cudaMemcpyHostToDevice), "H2D");
+    if (mode == 1) {
+        TV_CK(cudaMalloc(&d_pix.p, m * 8), "alloc");
+        TV_CK(cudaMalloc(&d_smp.p, m * 8), "alloc");
+        TV_CK(cudaMalloc(&d_fp.p, m * sizeof(tv_free_path)), "alloc");
+        if (n) TV_CK(cudaMemcpy(d_pix.p, pixels, n * 8, cudaMemcpyHostToDevice), "H2D");
+        if (n) TV_CK(cudaMemcpy(d_smp.p, samples, n * 8, cudaMemcpyHostToDevice), "H2D");
+    } else {
+        TV_CK(cudaMalloc(&d_tau.p, m * 8), "alloc");
+        TV_CK(cudaMalloc(&d_tr.p, m * 8), "alloc");
+    }
+    if (n) {
+        medium_kernel<<<static_cast<unsigned>((n + 127) / 128), 128>>>(
+            g.view, static_cast<const tv_ray*>(d_rays.p), n, mode, seed, static_cast<const uint64_t*>(d_pix.p),
+            static_cast<const uint64_t*>(d_smp.p), static_cast<double*>(d_tau.p), static_cast<double*>(d_tr.p),
+            static_cast<tv_free_path*>(d_fp.p), static_cast<unsigned long long*>(d_ctr.p));
+        TV_CK(cudaGetLastError(), "medium_kernel");
+    }
+    if (n && tau_out) TV_CK(cudaMemcpy(tau_out, d_tau.p, n * 8, cudaMemcpyDeviceToHost), "D2H");
+    if (n && trans_out) TV_CK(cudaMemcpy(trans_out, d_tr.p, n * 8, cudaMemcpyDeviceToHost), "D2H");
+    if (n && fp_out) TV_CK(cudaMemcpy(fp_out, d_fp.p, n * sizeof(tv_free_path), cudaMemcpyDeviceToHost), "D2H");
+    unsigned long long c[2];
+    TV_CK(cudaMemcpy(c, d_ctr.p, sizeof(c), cudaMemcpyDeviceToHost), "D2H");
+    if (stats) stats[0] = c[0], stats[1] = c[1];
+    return TV_OK;
+}
+}  // namespace
+
+int tv_march_transmittance(const tv_grid* h, const tv_ray* rays, uint64_t n, double* tau_out, double* trans_out,
+                           uint64_t stats[2]) {
+    return medium(h, rays, n, 0, 0, nullptr, nullptr, tau_out, trans_out, nullptr, stats);
+}
+
+int tv_sample_free_path(const tv_grid* h, const tv_ray* rays, uint64_t n, uint64_t seed, const uint64_t* pixels,
+                        const uint64_t* samples, tv_free_path* out, uint64_t stats[2]) {
+    return medium(h, rays, n, 1, seed, pixels, samples, nullptr, nullptr, out, stats);
+}
+
 int tv_locate_points(const tv_grid* h, const double* points, uint64_t n, uint32_t* out) {
     if (!h || ((!points || !out) && n)) return set_error(TV_ERR_ARG, "null argument");
     if (!n) return TV_OK;

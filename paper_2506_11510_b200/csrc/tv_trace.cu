@@ -190,6 +190,109 @@ __global__ void march_kernel(GridView G, const tv_ray* __restrict__ rays, uint64
     if (pass == 0) counts[i] = k;
 }
 
+// march_transmittance (mode 0) and sample_free_path (mode 1) (tracer.cpp:176-216)
+// over the same marcher as march_kernel; one thread per ray.
+__global__ void medium_kernel(GridView G, const tv_ray* __restrict__ rays, uint64_t n, int mode, uint64_t seed,
+                              const uint64_t* __restrict__ pixels, const uint64_t* __restrict__ samples,
+                              double* __restrict__ tau_out, double* __restrict__ trans_out,
+                              tv_free_path* __restrict__ fp_out, unsigned long long* counters) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const tv_ray R = rays[i];
+    const d3 o = mk(R.origin[0], R.origin[1], R.origin[2]);
+    const d3 dir = mk(R.dir[0], R.dir[1], R.dir[2]);
+    const double tmax = R.t_max;
+    double target = 0.0;
+    if (mode == 1) {  // sample_free_path draws its target first (tracer.cpp:190)
+        Rng rng;
+        rng.init(seed, pixels[i], samples[i]);
+        target = -log(1.0 - rng.next());
+    }
+    tv_free_path fp;
+    fp.collided = 0, fp.cell = kNone, fp.distance = 0.0;
+    fp.position[0] = o.x, fp.position[1] = o.y, fp.position[2] = o.z;
+    double tau = 0.0;
+    uint32_t visited = 0;
+    bool aborted = false;
+    double t0, t1;
+    uint32_t cell = kNone;
+    if (slab(o, dir, dmax(0.0, R.t_min), tmax, t0, t1)) {
+        d3 q = ray_at(o, dir, t0 + kNudge);
+        q = mk(dclamp(q.x, 0.0, 1.0), dclamp(q.y, 0.0, 1.0), dclamp(q.z, 0.0, 1.0));
+        cell = locate(G, q);
+    }
+    if (cell != kNone) {
+        double seg_start = t0, probe = t0 + kNudge, last_t1 = 0.0;
+        d3 event = o;
+        LeafRec rec = load_leaf(G.leaves, cell);
+        for (uint32_t steps = 1;; ++steps) {
+            if (steps > kMaxSteps) {
+                aborted = true;
+                break;
+            }
+            double t;
+            int slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+            if (slot < 0) {
+                probe += kNudge;
+                slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+                if (slot < 0) {
+                    aborted = true;
+                    break;
+                }
+            }
+            const double t_exit = dmax(probe + t, seg_start);
+            const double s0 = seg_start, lambda = static_cast<double>(__uint_as_float(rec.w[13]));
+            const uint32_t step_cell = cell;
+            double s1;
+            bool escaped = false;
+            if (t_exit >= tmax) {  // caller-imposed range ends inside the grid
+                s1 = tmax;
+                escaped = true;
+                event = ray_at(o, dir, tmax);
+            } else {
+                s1 = t_exit;
+                const uint32_t nb = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot) & kLeafIdxMask;
+                if (nb == kNoLeaf) {
+                    escaped = true;
+                    event = ray_at(o, dir, t_exit);
+                } else {
+                    rec = load_leaf(G.leaves, nb);
+                    cell = nb;
+                    seg_start = t_exit;
+                    probe = t_exit + kNudge;
+                }
+            }
+            ++visited;
+            const double seg_tau = lambda * (s1 - s0);
+            if (mode == 1 && lambda > 0.0 && tau + seg_tau >= target) {  // m.shorten (tracer.cpp:90-95)
+                const double dist = (target - tau) / lambda;
+                const d3 e = ray_at(o, dir, s0 + dist);
+                fp.collided = 1, fp.cell = G.leaf2tet[step_cell], fp.distance = s0 + dist;
+                fp.position[0] = e.x, fp.position[1] = e.y, fp.position[2] = e.z;
+                break;
+            }
+            tau += seg_tau;
+            last_t1 = s1;
+            if (escaped) break;
+        }
+        if (mode == 1 && !fp.collided) {
+            const d3 e = aborted ? ray_at(o, dir, last_t1) : event;
+            fp.position[0] = e.x, fp.position[1] = e.y, fp.position[2] = e.z;
+            fp.distance = last_t1;
+        }
+    }
+    if (counters) {
+        atomicAdd(counters, static_cast<unsigned long long>(visited));
+        if (aborted) atomicAdd(counters + 1, 1ull);
+    }
+    if (mode == 0) {
+        if (tau_out) tau_out[i] = tau;
+        if (trans_out) trans_out[i] = exp(-tau);
+    } else if (fp_out) {
+        fp_out[i] = fp;
+    }
+}
+
 __global__ void locate_kernel(GridView G, const double* __restrict__ pts, uint64_t n, uint32_t* __restrict__ out) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;

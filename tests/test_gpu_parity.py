@@ -234,3 +234,59 @@ def test_multi_batch_frame_matches_progressive_frames(tv, c1):
     assert np.array_equal(s.cpu().numpy().view(np.uint64), full.sum.view(np.uint64))
     assert np.array_equal(q.cpu().numpy().view(np.uint64), full.sum_sq.view(np.uint64))
     assert np.all(c.cpu().numpy() == spp) and full.paths_traced == w * h * spp
+
+
+def _media_grid(tv, steps=300, seed=0x61):
+    g = O.fuzzed(O.c_oracle(), steps, seed)
+    p = g.pools()
+    rng = np.random.default_rng(seed)
+    lm = p.leaf_mask
+    p.tets["density"][lm] = np.where(rng.random(lm.sum()) < 0.3, 0.0, rng.random(lm.sum()) * 6).astype(np.float32)
+    p.tets["mask"][lm] = 1
+    ref_g = O.from_pools(O.ref_oracle() or O.c_oracle(), p)
+    return p, ref_g, tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots, p.max_level)
+
+
+def test_march_transmittance(tv):
+    """tracer.cpp:176-187: the optical depth bit-exact (sequential sum over the
+    reference's segments), exp(-tau) within 2 ulp of the reference's std::exp."""
+    p, rg, dg = _media_grid(tv)
+    rays = O.random_cube_rays(7, 0x7472616e73, 3000)
+    rays[::3, 7] = rays[::3, 6] + 0.4  # finite t_max: clipped final segments
+    tau, tr, cells, deg = tv.march_transmittance(dg, rays)
+    cells_ref, t0, t1, off, _ = rg.march_segments(rays)
+    lam = p.tets["density"].astype(np.float64)
+    for i in range(len(rays)):
+        want = 0.0
+        for k in range(int(off[i]), int(off[i + 1])):
+            want += lam[cells_ref[k]] * (t1[k] - t0[k])
+        assert tau[i] == want, i
+        ref_t = rg.chk.fn("march_transmittance")(rg.h, rays[i].ctypes.data_as(O._D))
+        assert abs(tr[i] - ref_t) <= 2 * np.spacing(ref_t), i
+    assert cells == len(cells_ref) and deg == 0
+    vp = O.init_roots(O.c_oracle()).pools()
+    vac = tv.TetGrid.upload(vp.vq, vp.tets.view(tv.TET_DTYPE), vp.roots, 48)
+    _, tr0, _, _ = tv.march_transmittance(vac, rays[:50])
+    assert np.all(tr0 == 1.0)  # vacuum is exactly 1 (test_tracer.cpp:149-164)
+
+
+def test_sample_free_path(tv):
+    """tracer.cpp:189-216 against the reference, record for record."""
+    p, rg, dg = _media_grid(tv, 250, 0x62)
+    rays = O.random_cube_rays(9, 0x66726565, 2000)
+    rays[1::4, 7] = rays[1::4, 6] + 0.3
+    pix = np.arange(len(rays), dtype=np.uint64) * 7 + 3
+    smp = np.arange(len(rays), dtype=np.uint64) % 5
+    got = tv.sample_free_path(dg, rays, 11, pix, smp)
+    n_coll = 0
+    for i in range(len(rays)):
+        out = np.zeros(6)
+        rg.chk.fn("sample_free_path")(rg.h, rays[i].ctypes.data_as(O._D), 11, int(pix[i]), int(smp[i]),
+                                      out.ctypes.data_as(O._D))
+        assert bool(got["collided"][i]) == bool(out[0]), i
+        assert np.array_equal(got["position"][i], out[1:4]), i
+        assert got["distance"][i] == out[5], i
+        if out[0]:
+            n_coll += 1
+            assert got["cell"][i] == int(out[4]), i
+    assert 100 < n_coll < len(rays)
