@@ -321,7 +321,8 @@ def main():
     if os.path.exists(prof):
         try:
             pj = json.load(open(prof))
-            traffic = pj.get("dram_bytes_per_launch")
+            # ncu DRAM bytes per tet step at the bench config, scaled to this rank's launch
+            traffic = pj["dram_bytes_per_step"] * cells_rank
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
