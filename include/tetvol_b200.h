@@ -323,6 +323,10 @@ typedef struct {
     double position[3];
 } tv_free_path;
 
+/* trace(grid, ray, cfg, rng, stats) (tracer.hpp:78-79) per ray, with
+ * RngStream(seed, pixels[i], samples[i]); out_rgb: 3 doubles per ray. */
+int tv_trace_rays(const tv_grid* g, const tv_ray* rays, uint64_t n, const tv_render_config* cfg, uint64_t seed,
+                  const uint64_t* pixels, const uint64_t* samples, double* out_rgb, uint64_t stats[2]);
 /* march_transmittance (tracer.hpp:52) per ray: tau_out = the optical depth
  * (bit-exact), trans_out = exp(-tau); either may be NULL. stats (may be NULL):
  * cells_visited, degenerate_paths. */

@@ -202,6 +202,7 @@ class Checker:
               C.POINTER(_F))
             f("write_pfm", C.c_int, C.c_char_p, C.c_int, C.c_int, _D, _D, _U32, C.c_int)
             f("spot_rays", None, C.c_uint64, C.c_int, _D)
+            f("trace_ray", None, _P, _D, C.POINTER(RenderCfg), C.c_uint64, C.c_uint64, C.c_uint64, _D, _U64)
             f("spot_checks", None, _P, C.c_int, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int))
             f("read_pfm", C.c_int, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _F)
             f("trace_sample", None, _P, C.POINTER(Camera), C.POINTER(RenderCfg), C.c_int, C.c_int, C.c_int, _D, _U64)

@@ -419,6 +419,18 @@ void ref_spot_checks(void* h, int n, uint64_t seed, int* failures, int* first) {
     }
 }
 
+// tetvol::trace of one ray with RngStream(seed, pixel, sample); stats: cells, degenerate
+void ref_trace_ray(void* h, const double* r, const ref_render_cfg* c, uint64_t seed, uint64_t pixel, uint64_t sample,
+                   double* out, uint64_t* stats) {
+    Ray ray{v3(r), v3(r + 3), r[6], r[7]};
+    RngStream rng(seed, pixel, sample);
+    TraceStats st;
+    const Vec3 L = trace(*static_cast<TetGrid*>(h), ray, make_rc(c), rng, &st);
+    out[0] = L.x, out[1] = L.y, out[2] = L.z;
+    stats[0] += st.cells_visited;
+    stats[1] += st.degenerate_paths;
+}
+
 double ref_march_transmittance(void* h, const double* r) {
     Ray ray{v3(r), v3(r + 3), r[6], r[7]};
     return march_transmittance(*static_cast<TetGrid*>(h), ray);

@@ -170,6 +170,7 @@ _sig("tv_tile_unpack", C.c_int, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int
 _sig("tv_march_segments", C.c_int, _P, _P, C.c_uint64, _P, _U64, C.c_uint64, _U64, _U64)
 _sig("tv_locate_points", C.c_int, _P, _D, C.c_uint64, _U32)
 _sig("tv_march_transmittance", C.c_int, _P, _P, C.c_uint64, _D, _D, _U64)
+_sig("tv_trace_rays", C.c_int, _P, _P, C.c_uint64, C.POINTER(_RenderConfig), C.c_uint64, _U64, _U64, _D, _U64)
 _sig("tv_sample_free_path", C.c_int, _P, _P, C.c_uint64, C.c_uint64, _U64, _U64, _P, _U64)
 _sig("tv_render_regular", C.c_int, _F, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
      C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
@@ -462,6 +463,21 @@ def march_segments(grid: TetGrid, rays: np.ndarray):
 FREE_PATH_DTYPE = np.dtype([("collided", "<i4"), ("cell", "<u4"), ("distance", "<f8"), ("position", "<f8", 3)])
 
 
+def trace(grid: TetGrid, rays: np.ndarray, cfg: RenderConfig, seed: int, pixels, samples):
+    """tracer.hpp:78-79 over a batch, RngStream(seed, pixels[i], samples[i]) per ray.
+    -> ((n, 3) radiance, cells_visited, degenerate_paths)"""
+    r = np.ascontiguousarray(rays, np.float64).reshape(-1, 8)
+    px = np.ascontiguousarray(np.broadcast_to(pixels, len(r)), np.uint64)
+    sm = np.ascontiguousarray(np.broadcast_to(samples, len(r)), np.uint64)
+    out = np.zeros((len(r), 3))
+    st = np.zeros(2, np.uint64)
+    rc = cfg._c()
+    _check(_lib.tv_trace_rays(grid.handle, r.ctypes.data_as(_P), len(r), C.byref(rc), int(seed),
+                              px.ctypes.data_as(_U64), sm.ctypes.data_as(_U64), out.ctypes.data_as(_D),
+                              st.ctypes.data_as(_U64)))
+    return out, int(st[0]), int(st[1])
+
+
 def march_transmittance(grid: TetGrid, rays: np.ndarray):
     """tracer.hpp:52 over a batch -> (tau (bit-exact optical depth), exp(-tau), cells_visited, degenerate_paths)."""
     r = np.ascontiguousarray(rays, np.float64).reshape(-1, 8)
@@ -599,6 +615,6 @@ __all__ = [
     "ImageAccumulator", "IoError", "load_grid", "save_grid", "spot_rays",
     "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
     "build_adaptive_grid", "build_adaptive_grid_dev", "device_count", "generate_volume_dev", "locate_points",
-    "march_segments", "march_transmittance", "sample_free_path", "FREE_PATH_DTYPE", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",
+    "march_segments", "march_transmittance", "trace", "sample_free_path", "FREE_PATH_DTYPE", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",
     "tile_unpack", "version",
 ]

@@ -596,6 +596,43 @@ int medium(const tv_grid* h, const tv_ray* rays, uint64_t n, int mode, uint64_t 
 }
 }  // namespace
 
+int tv_trace_rays(const tv_grid* h, const tv_ray* rays, uint64_t n, const tv_render_config* cfg, uint64_t seed,
+                  const uint64_t* pixels, const uint64_t* samples, double* out_rgb, uint64_t stats[2]) {
+    if (!h || (n && (!rays || !pixels || !samples || !out_rgb))) return set_error(TV_ERR_ARG, "null argument");
+    int rc = validate_render(cfg);
+    if (rc) return rc;
+    const DeviceGrid& g = h->g;
+    if ((rc = use_device(g.device))) return rc;
+    struct Dev {
+        void* p = nullptr;
+        ~Dev() {
+            if (p) cudaFree(p);
+        }
+    } d_rays, d_pix, d_smp, d_out, d_ctr;
+    const uint64_t m = n ? n : 1;
+    TV_CK(cudaMalloc(&d_rays.p, m * sizeof(tv_ray)), "alloc");
+    TV_CK(cudaMalloc(&d_pix.p, m * 8), "alloc");
+    TV_CK(cudaMalloc(&d_smp.p, m * 8), "alloc");
+    TV_CK(cudaMalloc(&d_out.p, m * 24), "alloc");
+    TV_CK(cudaMalloc(&d_ctr.p, 16), "alloc");
+    TV_CK(cudaMemset(d_ctr.p, 0, 16), "memset");
+    if (n) {
+        TV_CK(cudaMemcpy(d_rays.p, rays, n * sizeof(tv_ray), cudaMemcpyHostToDevice), "H2D");
+        TV_CK(cudaMemcpy(d_pix.p, pixels, n * 8, cudaMemcpyHostToDevice), "H2D");
+        TV_CK(cudaMemcpy(d_smp.p, samples, n * 8, cudaMemcpyHostToDevice), "H2D");
+        trace_rays_kernel<<<static_cast<unsigned>((n + 127) / 128), 128>>>(
+            g.view, make_params(cfg), static_cast<const tv_ray*>(d_rays.p), n, seed,
+            static_cast<const uint64_t*>(d_pix.p), static_cast<const uint64_t*>(d_smp.p),
+            static_cast<double*>(d_out.p), static_cast<unsigned long long*>(d_ctr.p));
+        TV_CK(cudaGetLastError(), "trace_rays_kernel");
+        TV_CK(cudaMemcpy(out_rgb, d_out.p, n * 24, cudaMemcpyDeviceToHost), "D2H");
+    }
+    unsigned long long c[2];
+    TV_CK(cudaMemcpy(c, d_ctr.p, sizeof(c), cudaMemcpyDeviceToHost), "D2H");
+    if (stats) stats[0] = c[0], stats[1] = c[1];
+    return TV_OK;
+}
+
 int tv_march_transmittance(const tv_grid* h, const tv_ray* rays, uint64_t n, double* tau_out, double* trans_out,
                            uint64_t stats[2]) {
     return medium(h, rays, n, 0, 0, nullptr, nullptr, tau_out, trans_out, nullptr, stats);

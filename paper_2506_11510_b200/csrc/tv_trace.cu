@@ -293,6 +293,122 @@ __global__ void medium_kernel(GridView G, const tv_ray* __restrict__ rays, uint6
     }
 }
 
+// tetvol::trace (tracer.cpp:258-263) = trace_path (path_integrator.hpp:42-84)
+// for arbitrary rays, one thread per ray, RngStream(seed, pixels[i], samples[i]).
+// The first flight honours the ray's [t_min, t_max]; redirects reset it to
+// [0, inf) (TetMarcher::redirect, tracer.cpp:97-105).
+__global__ void trace_rays_kernel(GridView G, RenderParams P, const tv_ray* __restrict__ rays, uint64_t n,
+                                  uint64_t seed, const uint64_t* __restrict__ pixels,
+                                  const uint64_t* __restrict__ samples, double* __restrict__ out,
+                                  unsigned long long* counters) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const tv_ray R = rays[i];
+    d3 o = mk(R.origin[0], R.origin[1], R.origin[2]);
+    d3 dir = mk(R.dir[0], R.dir[1], R.dir[2]);
+    double tmax = R.t_max;
+    Rng rng;
+    rng.init(seed, pixels[i], samples[i]);
+    d3 radiance = mk(0, 0, 0), throughput = mk(1, 1, 1);
+    uint32_t visited = 0;
+    bool degenerate = false;
+    double t0, t1;
+    uint32_t cell = kNone;
+    if (slab(o, dir, dmax(0.0, R.t_min), tmax, t0, t1)) {
+        d3 q = ray_at(o, dir, t0 + kNudge);
+        q = mk(dclamp(q.x, 0.0, 1.0), dclamp(q.y, 0.0, 1.0), dclamp(q.z, 0.0, 1.0));
+        cell = locate(G, q);
+    }
+    if (cell == kNone) {
+        radiance = mk(P.env[0], P.env[1], P.env[2]);  // !m.start(primary): return environment
+    } else {
+        double seg_start = t0, probe = t0 + kNudge;
+        LeafRec rec = load_leaf(G.leaves, cell);
+        uint32_t steps = 0;
+        for (int bounce = 0;;) {
+            const double target = -log(1.0 - rng.next());
+            double tau = 0.0;
+            bool collided = false, aborted = false;
+            d3 event = o;
+            for (;;) {  // TetMarcher::next until escape / abort / collision
+                if (++steps > kMaxSteps) {
+                    aborted = true;
+                    break;
+                }
+                double t;
+                int slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+                if (slot < 0) {
+                    probe += kNudge;
+                    slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+                    if (slot < 0) {
+                        aborted = true;
+                        break;
+                    }
+                }
+                const double t_exit = dmax(probe + t, seg_start);
+                const double s0 = seg_start, lambda = static_cast<double>(__uint_as_float(rec.w[13]));
+                bool escaped = false;
+                double s1 = t_exit;
+                uint32_t next = kNoLeaf;
+                if (t_exit >= tmax) {
+                    s1 = tmax;
+                    escaped = true;
+                } else {
+                    next = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot) & kLeafIdxMask;
+                    escaped = next == kNoLeaf;
+                }
+                ++visited;
+                const double seg_tau = lambda * (s1 - s0);
+                if (lambda > 0.0 && tau + seg_tau >= target) {  // m.shorten: stay in this cell
+                    event = ray_at(o, dir, s0 + (target - tau) / lambda);
+                    collided = true;
+                    break;
+                }
+                tau += seg_tau;
+                if (escaped) break;
+                rec = load_leaf(G.leaves, next);
+                cell = next;
+                seg_start = t_exit;
+                probe = t_exit + kNudge;
+            }
+            if (aborted) {
+                degenerate = true;
+                break;
+            }
+            if (!collided) {
+                radiance = add(radiance, mulv(throughput, mk(P.env[0], P.env[1], P.env[2])));
+                break;
+            }
+            const uint32_t mask = rec.w[12] >> 24;
+            if (mask & 2u) {
+                const d3 e = emission_color(static_cast<double>(__uint_as_float(rec.w[14])));
+                radiance = add(radiance, mul(mulv(throughput, e), P.emission_scale));
+            }
+            throughput = mul(throughput, (mask & 4u) ? static_cast<double>(__uint_as_float(rec.w[15])) : P.default_albedo);
+            ++bounce;
+            if (bounce >= P.max_bounces) break;
+            if (bounce >= 4) {
+                const double pm = dmax(throughput.x, dmax(throughput.y, throughput.z));
+                if (pm < 1e-3) {
+                    if (rng.next() >= pm) break;
+                    throughput = divs(throughput, pm);
+                }
+            }
+            // TetMarcher::redirect: from the event point, [0, inf), same cell
+            dir = sample_phase_hg(dir, P.g, rng);
+            o = event;
+            tmax = __longlong_as_double(0x7ff0000000000000ll);
+            seg_start = 0.0;
+            probe = 0.0;
+        }
+    }
+    out[3 * i] = radiance.x, out[3 * i + 1] = radiance.y, out[3 * i + 2] = radiance.z;
+    if (counters) {
+        atomicAdd(counters, static_cast<unsigned long long>(visited));
+        if (degenerate) atomicAdd(counters + 1, 1ull);
+    }
+}
+
 __global__ void locate_kernel(GridView G, const double* __restrict__ pts, uint64_t n, uint32_t* __restrict__ out) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;

@@ -51,6 +51,9 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* cells, const do
 __global__ void march_kernel(GridView G, const tv_ray* rays, uint64_t n, int pass, uint64_t* counts,
                              const uint64_t* offsets, tv_segment* out, uint64_t cap, unsigned long long* deg);
 __global__ void locate_kernel(GridView G, const double* pts, uint64_t n, uint32_t* out);
+__global__ void trace_rays_kernel(GridView G, RenderParams P, const tv_ray* rays, uint64_t n, uint64_t seed,
+                                  const uint64_t* pixels, const uint64_t* samples, double* out,
+                                  unsigned long long* counters);
 __global__ void medium_kernel(GridView G, const tv_ray* rays, uint64_t n, int mode, uint64_t seed,
                               const uint64_t* pixels, const uint64_t* samples, double* tau_out, double* trans_out,
                               tv_free_path* fp_out, unsigned long long* counters);

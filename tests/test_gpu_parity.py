@@ -290,3 +290,40 @@ def test_sample_free_path(tv):
             n_coll += 1
             assert got["cell"][i] == int(out[4]), i
     assert 100 < n_coll < len(rays)
+
+
+def test_trace_rays_matches_reference_trace(tv):
+    """tetvol::trace (tracer.cpp:258-263) for arbitrary rays, incl. finite t_max
+    and rays starting inside the cube, with emission and albedo channels."""
+    ref = O.ref_oracle()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    g = O.fuzzed(O.c_oracle(), 300, 0x71)
+    p = g.pools()
+    rng = np.random.default_rng(71)
+    lm = p.leaf_mask
+    n = int(lm.sum())
+    p.tets["density"][lm] = (rng.random(n) * 5).astype(np.float32)
+    p.tets["temperature"][lm] = rng.random(n).astype(np.float32)
+    p.tets["albedo"][lm] = rng.random(n).astype(np.float32)
+    p.tets["mask"][lm] = np.where(rng.random(n) < 0.5, 7, 1).astype(np.uint8)
+    dg = tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots, p.max_level)
+    rg = O.from_pools(ref, p)
+    rays = O.random_cube_rays(4, 0x7472616365, 1500)
+    rays[::5, 7] = rays[::5, 6] + 0.35
+    rays[1::7, 0:3] = rng.random((len(rays[1::7]), 3))  # origins inside the cube
+    cfg = dict(spp=1, max_bounces=24, seed=0, hg_g=0.4, default_albedo=0.7, env=(1.0, 0.5, 0.25),
+               emission_scale=2.0)
+    rc = tv.RenderConfig(max_bounces=24, hg_g=0.4, default_albedo=0.7, environment=(1.0, 0.5, 0.25),
+                         emission_scale=2.0)
+    pix = np.arange(len(rays), dtype=np.uint64) * 3 + 1
+    smp = np.arange(len(rays), dtype=np.uint64) % 7
+    got, cells, deg = tv.trace(dg, rays, rc, 5, pix, smp)
+    orc = O.render_cfg(**cfg)
+    st = np.zeros(2, np.uint64)
+    for i in range(len(rays)):
+        out = np.zeros(3)
+        ref.fn("trace_ray")(rg.h, rays[i].ctypes.data_as(O._D), O.C.byref(orc), 5, int(pix[i]), int(smp[i]),
+                            out.ctypes.data_as(O._D), st.ctypes.data_as(O._U64))
+        assert np.array_equal(got[i].view(np.uint64), out.view(np.uint64)), (i, got[i], out)
+    assert cells == int(st[0]) and deg == int(st[1])
