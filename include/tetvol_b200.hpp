@@ -206,4 +206,57 @@ inline std::vector<std::vector<RaySegment>> march_segments(const DeviceGrid& gri
     return out;
 }
 
+inline std::vector<tv_ray> to_c(const std::vector<Ray>& rays) {
+    std::vector<tv_ray> rr(rays.size());
+    for (size_t i = 0; i < rays.size(); ++i) {
+        const Ray& r = rays[i];
+        rr[i] = tv_ray{{r.origin.x, r.origin.y, r.origin.z}, {r.dir.x, r.dir.y, r.dir.z}, r.t_min, r.t_max};
+    }
+    return rr;
+}
+
+// march_transmittance (tracer.hpp:52), batched
+inline std::vector<double> march_transmittance(const DeviceGrid& grid, const std::vector<Ray>& rays,
+                                               TraceStats* stats = nullptr) {
+    const auto rr = to_c(rays);
+    std::vector<double> out(rays.size());
+    uint64_t st[2] = {0, 0};
+    check(tv_march_transmittance(grid.handle(), rr.data(), rr.size(), nullptr, out.data(), st));
+    if (stats) stats->cells_visited += st[0], stats->degenerate_paths += st[1];
+    return out;
+}
+
+// trace / sample_free_path (tracer.hpp:63, 78-79), batched; ray i uses RngStream(seed, pixels[i], samples[i])
+inline std::vector<Vec3> trace(const DeviceGrid& grid, const std::vector<Ray>& rays, const RenderConfig& cfg,
+                               uint64_t seed, const std::vector<uint64_t>& pixels,
+                               const std::vector<uint64_t>& samples, TraceStats* stats = nullptr) {
+    const auto rr = to_c(rays);
+    const tv_render_config rc = to_c(cfg);
+    std::vector<double> rgb(3 * rays.size());
+    uint64_t st[2] = {0, 0};
+    check(tv_trace_rays(grid.handle(), rr.data(), rr.size(), &rc, seed, pixels.data(), samples.data(), rgb.data(), st));
+    if (stats) stats->cells_visited += st[0], stats->degenerate_paths += st[1];
+    std::vector<Vec3> out(rays.size());
+    for (size_t i = 0; i < rays.size(); ++i) out[i] = Vec3{rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]};
+    return out;
+}
+
+inline std::vector<FreePathSample> sample_free_path(const DeviceGrid& grid, const std::vector<Ray>& rays,
+                                                    uint64_t seed, const std::vector<uint64_t>& pixels,
+                                                    const std::vector<uint64_t>& samples,
+                                                    TraceStats* stats = nullptr) {
+    const auto rr = to_c(rays);
+    std::vector<tv_free_path> fp(rays.size());
+    uint64_t st[2] = {0, 0};
+    check(tv_sample_free_path(grid.handle(), rr.data(), rr.size(), seed, pixels.data(), samples.data(), fp.data(), st));
+    if (stats) stats->cells_visited += st[0], stats->degenerate_paths += st[1];
+    std::vector<FreePathSample> out(rays.size());
+    for (size_t i = 0; i < rays.size(); ++i) {
+        out[i].collided = fp[i].collided != 0;
+        out[i].position = Vec3{fp[i].position[0], fp[i].position[1], fp[i].position[2]};
+        out[i].cell = fp[i].cell;
+        out[i].distance = fp[i].distance;
+    }
+    return out;
+}
 }  // namespace tetvol::b200

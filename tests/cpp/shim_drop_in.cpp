@@ -144,6 +144,26 @@ int main() {
         std::remove(p2.c_str());
     }
 
+    // trace / transmittance / free path agree with the reference entry points
+    {
+        std::vector<Ray> rr(rays.begin(), rays.begin() + 100);
+        std::vector<uint64_t> px(rr.size()), sm(rr.size());
+        for (size_t i = 0; i < rr.size(); ++i) px[i] = 5 * i + 1, sm[i] = i % 3;
+        RenderConfig tc;
+        tc.max_bounces = 12;
+        auto L = b200::trace(dg, rr, tc, 9, px, sm);
+        auto T = b200::march_transmittance(dg, rr);
+        auto F = b200::sample_free_path(dg, rr, 9, px, sm);
+        for (size_t i = 0; i < rr.size(); ++i) {
+            RngStream r1(9, px[i], sm[i]), r2(9, px[i], sm[i]);
+            const Vec3 want = trace(ref, rr[i], tc, r1);
+            REQUIRE(std::memcmp(&want, &L[i], sizeof(Vec3)) == 0);
+            REQUIRE(std::fabs(T[i] - march_transmittance(ref, rr[i])) <= 4e-16 * std::fabs(T[i]) + 1e-300);
+            const FreePathSample f = sample_free_path(ref, rr[i], r2);
+            REQUIRE(f.collided == F[i].collided && f.distance == F[i].distance && f.cell == F[i].cell);
+        }
+    }
+
     // exceptions map back to the reference types
     try {
         RenderConfig bad;
