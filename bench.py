@@ -99,12 +99,18 @@ CPU_SPP = 8  # cpu_baseline sample: ~10 s of host work on 16 cores
 REF_SPP = 4  # --impl reference: samples per pixel per timed step
 
 
-def cpu_render_sample(v, t, r, max_level, threads=0):
-    """The reference renderer (oracle/_ref) on the same grid and frame, spp = CPU_SPP."""
+def cpu_render_sample(v, t, r, max_level, threads=0, padded=False):
+    """The reference renderer (oracle/_ref) on the same grid and frame, spp = CPU_SPP.
+    padded=True uses oracle/_ref/pad (alignas(64) TraceStats); None if absent."""
     import oracle as O
 
-    chk = O.ref_oracle()
-    kind = "reference"
+    if padded:
+        chk, kind = O.ref_pad_oracle(), "reference"
+        if chk is None:
+            return None, kind, 0
+    else:
+        chk = O.ref_oracle()
+        kind = "reference"
     if chk is None:
         chk, kind = O.c_oracle(), "port"
     g = O.from_pools(chk, O.Pools(v, t.view(O.TET_DTYPE), r, max_level))
@@ -340,6 +346,14 @@ def main():
             cpu = {"value": npx * CPU_SPP / out["seconds"], "unit": "samples/s", "cores": cores, "kind": kind,
                    "sample": f"1024x1024 x {CPU_SPP} spp of the same C2 frame (first samples per pixel), threads=all",
                    "seconds": out["seconds"], "tet_steps_per_s": out["cells_visited"] / out["seconds"]}
+            # the shipped build false-shares its per-thread counters;
+            # the same sources with alignas(64) TraceStats are the fair CPU figure.
+            po, _, _ = cpu_render_sample(v, t, r, BUILD["max_level"], padded=True)
+            if po is not None:
+                cpu["padded"] = {
+                    "value": npx * CPU_SPP / po["seconds"], "unit": "samples/s", "cores": cores,
+                    "seconds": po["seconds"], "tet_steps_per_s": po["cells_visited"] / po["seconds"],
+                    "build": "oracle/_ref/pad: reference sources with struct alignas(64) TraceStats"}
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": "failed", "error": repr(e)}

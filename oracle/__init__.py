@@ -330,6 +330,18 @@ def ref_oracle() -> Checker | None:
     return _REF
 
 
+_REF_PAD = None
+
+
+def ref_pad_oracle() -> Checker | None:
+    """The reference built with ``struct alignas(64) TraceStats``,
+    or None when it was never built. Used only for bench.py's cpu_baseline."""
+    global _REF_PAD
+    if _REF_PAD is None:
+        _REF_PAD = _lib_or_none(os.path.join(HERE, "_ref", "pad", "libtetvol_ref_pad.so"), "ref")
+    return _REF_PAD
+
+
 def gen_volume(kind: str, n: int, value: float = 1.0) -> np.ndarray:
     kinds = {"constant": 0, "ramp": 1, "blob": 2, "step": 3, "noise": 4, "cloud": 5}
     out = np.zeros((n, n, n), np.float32)

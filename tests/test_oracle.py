@@ -334,3 +334,20 @@ def test_dvol_restatement_matches_reference(tmp_path):
     data = (F * 3)(*[v.ctypes.data_as(F) for v in chans.values()])
     assert ref.fn("dvol_save")(fn.encode(), *dims, 3, names, data) == 0
     assert dvol_bytes(dims, chans) == open(fn, "rb").read()
+
+
+@pytest.mark.skipif(O.ref_pad_oracle() is None or ref is None, reason="oracle/_ref/pad not built")
+def test_padded_reference_build_renders_identically():
+    """oracle/_ref/pad (alignas(64) TraceStats) only changes the
+    counter layout: the multi-threaded render is bit-identical to the shipped one."""
+    vol = O.gen_volume("cloud", 32)
+    cam = O.camera((0.5, 0.5, -1.2), (0, 0, 1), (0, 1, 0), 40, 48, 40)
+    outs = []
+    for chk in (ref, O.ref_pad_oracle()):
+        g, _ = O.build(chk, vol, O.build_cfg(0.15, 24, True, 1.0, 16.0), cam)
+        outs.append(g.render(cam, O.render_cfg(spp=2, max_bounces=16), 4))
+    a, b = outs
+    assert a["cells_visited"] == b["cells_visited"]
+    for k in ("sum", "sum_sq", "counts"):
+        if k in a:
+            assert np.array_equal(a[k], b[k])
