@@ -76,7 +76,7 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
     for (int f = 0; f < 4; ++f) {
         const uint32_t nb = tt.neighbors[f];
         const uint32_t id = static_cast<uint32_t>(tt.normal_ids[f]) & 31u;
-        r.w[f] = (nb == kNone ? kNoLeaf : tet2leaf[nb]) | (id << 27);
+        r.w[f] = nbr_word(nb == kNone ? kNoLeaf : tet2leaf[nb], id);
         // exit_face reads vertex verts[(f+1)&3] of face f (tracer.cpp:152)
         const uint4 q = verts[tt.verts[(f + 1) & 3]];
         const uint32_t qq[3] = {q.x, q.y, q.z};

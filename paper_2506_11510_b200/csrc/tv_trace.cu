@@ -169,7 +169,7 @@ __global__ void march_kernel(GridView G, const tv_ray* __restrict__ rays, uint64
                 }
                 const double t_exit = dmax(probe + t, seg_start);
                 const bool clip = t_exit >= tmax;
-                const uint32_t nb = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot) & kLeafIdxMask;
+                const uint32_t nb = nbr_leaf(sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot));
                 if (pass && base + k < cap) {
                     tv_segment sgm;
                     sgm.cell = G.leaf2tet[cell];
@@ -251,7 +251,7 @@ __global__ void medium_kernel(GridView G, const tv_ray* __restrict__ rays, uint6
                 event = ray_at(o, dir, tmax);
             } else {
                 s1 = t_exit;
-                const uint32_t nb = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot) & kLeafIdxMask;
+                const uint32_t nb = nbr_leaf(sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot));
                 if (nb == kNoLeaf) {
                     escaped = true;
                     event = ray_at(o, dir, t_exit);
@@ -354,7 +354,7 @@ __global__ void trace_rays_kernel(GridView G, RenderParams P, const tv_ray* __re
                     s1 = tmax;
                     escaped = true;
                 } else {
-                    next = sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot) & kLeafIdxMask;
+                    next = nbr_leaf(sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot));
                     escaped = next == kNoLeaf;
                 }
                 ++visited;
