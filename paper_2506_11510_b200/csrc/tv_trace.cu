@@ -85,7 +85,10 @@ __global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, Sta
         } else {
             t0 = 0.0;
         }
-        st[p] = StartRec{dir.x, dir.y, dir.z, t0};
+        // the first target is drawn here, in the fully populated start kernel,
+        // instead of in the trace kernel's divergent regeneration branch
+        const double target = -log(1.0 - rng.next());
+        st[p] = StartRec{dir.x, dir.y, dir.z, t0, rng.key, target};
         cells[p] = cell;
     }
 }

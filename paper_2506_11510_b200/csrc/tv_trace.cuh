@@ -32,6 +32,8 @@ struct Batch {
 
 struct StartRec {  // camera ray of one path after TetMarcher::start
     double dx, dy, dz, t0;
+    unsigned long long key;  // the path's RngStream key (rng.hpp:19-22)
+    double target;           // first optical-depth target, -log(1 - u) at dim 3 (path_integrator.hpp:49)
 };
 
 struct RenderOut {
