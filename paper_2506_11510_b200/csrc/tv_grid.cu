@@ -84,6 +84,8 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
         pos2_axes(id, ai, aj);
         r.w[4 + 2 * f] = __float_as_uint(static_cast<float>(qq[ai]) * 0x1.0p-24f);
         r.w[5 + 2 * f] = __float_as_uint(static_cast<float>(qq[aj]) * 0x1.0p-24f);
+        // the sign of m1 rides in c1's (otherwise zero) sign bit; see exit_face_nbr
+        if (pos2_code(id) & 16u) r.w[5 + 2 * f] |= 0x80000000u;
         codes |= pos2_code(id) << (6 * f);
     }
     r.w[12] = codes | (static_cast<uint32_t>(tt.mask & 7u) << 24);
