@@ -179,23 +179,21 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaEventCreate(&w.ev1), "event create");
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
         // tuning knobs (defaults are the measured best on B200)
-        const int slots = 1;
-        const int maxreg = env_int("TV_TRACE_MAXREG", 128);
-        w.trace = trace_variant(maxreg, slots, w.trace_threads);
+        const int maxreg = env_int("TV_TRACE_MAXREG", 72);
+        w.trace = trace_variant(maxreg, env_int("TV_TRACE_THREADS", 128), w.trace_threads);
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 2));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
         int per_sm = 1;
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
-                             env_int("TV_CARVEOUT", 50));
+                             env_int("TV_CARVEOUT", 72));
         cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace),
                                                       w.trace_threads, 0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
         if (env_int("TV_VERBOSE", 0))
-            std::fprintf(stderr, "tetvol_b200: trace kernel maxreg=%d slots=%d, %d blocks/SM resident, %d blocks\n", maxreg,
-                         slots, per_sm,
-                         w.trace_blocks);
+            std::fprintf(stderr, "tetvol_b200: trace kernel maxreg=%d threads=%d, %d blocks/SM resident, %d blocks\n",
+                         maxreg, w.trace_threads, per_sm, w.trace_blocks);
     }
     out = &w;
     return TV_OK;
