@@ -55,6 +55,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
+        self.window = None  # (t0, t1) host monotonic bounds of the timed region
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -66,6 +67,10 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # started ahead of the timed region; wait until it is sampling
+            t_end = time.monotonic() + 5.0
+            while not self.rows and time.monotonic() < t_end and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
@@ -74,7 +79,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append(parts + [time.monotonic()])
 
     def __exit__(self, *a):
         if self.proc:
@@ -85,14 +90,17 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        if self.window is not None:  # only the samples taken inside the timed region
+            rows = [r for r in rows if self.window[0] <= r[7] <= self.window[1]]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
 
 
 CPU_SPP = 8  # cpu_baseline sample: ~10 s of host work on 16 cores
@@ -246,6 +254,7 @@ def main():
                 tv.tile_unpack(gathered[r * words:(r + 1) * words].data_ptr(), sum_.data_ptr(), W_IMG, H_IMG, r,
                                world, 3, sh)
 
+    clk = ClockSampler(dev).__enter__()  # sampling (every 100 ms) from before the warm-up
     for i in range(args.warmup):
         step(i)
     stream.synchronize()
@@ -255,12 +264,15 @@ def main():
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
-        t0.record(stream)
-        for i in range(args.steps):
-            step(i, timed=True)
-        t1.record(stream)
-        stream.synchronize()
+    h0 = time.monotonic()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(i, timed=True)
+    t1.record(stream)
+    stream.synchronize()
+    clk.window = (h0, time.monotonic())
+    time.sleep(0.15)  # let the sample covering the region's end arrive
+    clk.__exit__(None, None, None)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
     kern_ms = float(np.mean([k_start[i].elapsed_time(k_end[i]) for i in range(args.steps)]))
