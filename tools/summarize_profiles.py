@@ -45,7 +45,7 @@ def dram(steps):
     hdr = {h: i for i, h in enumerate(rows[h0])}
     m = {r[hdr["Metric Name"]]: float(r[hdr["Metric Value"]].replace(",", "")) for r in rows[h0 + 1:] if len(r) > 5}
     rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
-    out = {"kernel": "trace_kernel_t<128, 1, 128>", "config": "C2 1024x1024 x 32 spp (bench.py workload)",
+    out = {"kernel": "trace_kernel_t<72, 1, 128>", "config": "C2 1024x1024 x 32 spp (bench.py workload)",
            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
            "tet_steps_per_launch": steps, "dram_bytes_per_step": (rd + wr) / steps,
            "l2_bytes_per_step": m["lts__t_sectors.sum"] * 32 / steps,
