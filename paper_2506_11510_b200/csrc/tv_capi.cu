@@ -181,7 +181,7 @@ int workspace(int device, Workspace*& out) {
         // tuning knobs (defaults are the measured best on B200)
         const int maxreg = env_int("TV_TRACE_MAXREG", 72);
         w.trace = trace_variant(maxreg, env_int("TV_TRACE_THREADS", 128), w.trace_threads);
-        w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 4));
+        w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 5));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 2));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
         int per_sm = 1;
