@@ -117,7 +117,21 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
             if (O.sum_sq) qr = O.sum_sq[3 * pix], qg = O.sum_sq[3 * pix + 1], qb = O.sum_sq[3 * pix + 2];
             if (O.counts) n = O.counts[pix];
         }
-        for (uint32_t k = 0; k < B.ns; ++k) {
+        uint32_t k = 0;
+        if (B.order && !(p0 & 1u)) {
+            // sample-major order: the pixel's samples are consecutive paths, so two
+            // samples (48 B) are three aligned 16-B loads; summation order unchanged
+            const double2* r2 = reinterpret_cast<const double2*>(rad + 3ull * p0);
+            for (; k + 1 < B.ns; k += 2) {
+                const double2 a = r2[3 * (k >> 1)], b2 = r2[3 * (k >> 1) + 1], c2 = r2[3 * (k >> 1) + 2];
+                sr += a.x, sg += a.y, sb += b2.x;
+                qr += a.x * a.x, qg += a.y * a.y, qb += b2.x * b2.x;
+                sr += b2.y, sg += c2.x, sb += c2.y;
+                qr += b2.y * b2.y, qg += c2.x * c2.x, qb += c2.y * c2.y;
+                n += 2;
+            }
+        }
+        for (; k < B.ns; ++k) {
             const uint64_t pp = path_id(B, unit, lane, k);
             const double r = rad[3 * pp], g = rad[3 * pp + 1], b = rad[3 * pp + 2];
             sr += r, sg += g, sb += b;
