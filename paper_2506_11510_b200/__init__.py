@@ -374,7 +374,8 @@ class TetGrid:
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.tv_grid_free(self._h)
+            if _lib is not None:  # None only during interpreter shutdown
+                _lib.tv_grid_free(self._h)
             self._h = None
 
     def __del__(self):

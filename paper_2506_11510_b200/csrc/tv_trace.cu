@@ -48,7 +48,7 @@ __device__ __forceinline__ void path_pixel(const Batch& B, uint32_t p, int& px, 
         lane = r & 31u;
     }
     const uint32_t k = unit >> 3, sub = unit & 7u;
-    const uint32_t t = static_cast<uint32_t>(B.rank) + k * static_cast<uint32_t>(B.n_ranks);
+    const uint32_t t = B.tile_order ? B.tile_order[k] : static_cast<uint32_t>(B.rank) + k * static_cast<uint32_t>(B.n_ranks);
     const uint32_t tx = t % B.tiles_x, ty = t / B.tiles_x;
     px = static_cast<int>(tx * 16 + (sub & 1u) * 8 + (lane & 7u));
     py = static_cast<int>(ty * 16 + (sub >> 1) * 4 + (lane >> 3));

@@ -28,6 +28,7 @@ struct Batch {
     uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
     uint32_t regen_min, scatter_min;  // warp-batching thresholds of the trace loop
     uint32_t order;                   // path id order (see path_id in tv_trace.cu)
+    const uint32_t* tile_order;       // this rank's tiles in processing order (null: t = rank + k * n_ranks)
 };
 
 struct StartRec {  // camera ray of one path after TetMarcher::start

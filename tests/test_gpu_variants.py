@@ -23,6 +23,8 @@ CONFIGS = [
     {"TV_REGEN_MIN": "32", "TV_SCATTER_MIN": "32"},
     {"TV_ORDER": "0"},
     {"TV_CARVEOUT": "50"},
+    {"TV_TILE_ORDER": "2"},
+    {"TV_TILE_ORDER": "2", "TV_TILE_RADIUS_PCT": "30"},
 ]
 
 
