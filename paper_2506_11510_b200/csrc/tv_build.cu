@@ -925,24 +925,6 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    {
-        // map the build's memory pool once, up front, in one block sized from
-        // the volume (480 B per voxel, at most 12 GB): growing it buffer by
-        // buffer maps and scrubs fresh device memory a piece at a time (the
-        // first build of a C2 grid: 0.73 -> 0.23 s wall). Issued after the
-        // build's start event.
-        cudaMemPool_t pool;
-        uint64_t have = 0;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess &&
-            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have) == cudaSuccess) {
-            const uint64_t want = std::min<uint64_t>(static_cast<uint64_t>(nx) * ny * nz * 480ull, 12ull << 30);
-            if (have < want) {
-                void* p = nullptr;
-                if (cudaMallocAsync(&p, want - have, 0) == cudaSuccess) cudaFreeAsync(p, 0);
-                else cudaGetLastError();
-            }
-        }
-    }
 
     const uint64_t nvox = static_cast<uint64_t>(nx) * ny * nz;
     VolView V{dens, temp, alb, nx, ny, nz};
