@@ -252,6 +252,17 @@ int tv_tile_pack(const void* frame_dev, void* packed_dev, int32_t width, int32_t
                  int32_t n_ranks, int32_t elem_words, void* stream);
 int tv_tile_unpack(const void* packed_dev, void* frame_dev, int32_t width, int32_t height, int32_t rank,
                    int32_t n_ranks, int32_t elem_words, void* stream);
+/* Direct peer writes (the gather fused into the render's accumulate step):
+ * rank 0 exports its full-frame accumulators, every other rank maps them and
+ * passes the mapped pointers to tv_render_tiles, whose accumulate kernel then
+ * stores this rank's pixels straight into rank 0's HBM over NVLink (no pack,
+ * all-gather or unpack). tv_render_tiles detects peer outputs and ends the
+ * accumulate kernel with a system-scope fence, so a stream-ordered barrier
+ * after it (e.g. a one-word NCCL all-reduce) publishes the pixels. The handle
+ * is 64 opaque bytes (cudaIpcMemHandle_t). */
+int tv_ipc_export(const void* dev_ptr, uint8_t handle[64]);
+int tv_ipc_open(const uint8_t handle[64], int device, void** dev_ptr_out);
+int tv_ipc_close(void* dev_ptr);
 
 /* -- volumes in HBM (DenseVolume, volume.hpp:19-58; .dvol, volume.cpp:84-138) -- */
 /* create: a zero "density" channel (volume.hpp:25); dims in [1, 4096].       */

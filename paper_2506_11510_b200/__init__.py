@@ -177,6 +177,12 @@ _sig("tv_render_regular", C.c_int, _F, C.c_int32, C.c_int32, C.c_int32, C.c_doub
 _sig("tv_render_regular_dev", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
      C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
 
+_sig("tv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8))
+_sig("tv_ipc_open", C.c_int, C.POINTER(C.c_uint8), C.c_int, C.POINTER(_P))
+_sig("tv_ipc_close", C.c_int, _P)
+_sig("tv_diag_gather_ceiling", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.c_int,
+     C.POINTER(C.c_double))
+
 # reference Tet layout (tet_grid.hpp:64-75; 68 bytes)
 TET_DTYPE = np.dtype([("verts", "<u4", 4), ("children", "<u4", 2), ("parent", "<u4"), ("neighbors", "<u4", 4),
                       ("normal_ids", "u1", 4), ("level", "u1"), ("pad0", "u1", 3), ("density", "<f4"),
@@ -428,6 +434,35 @@ def last_frame_timing(device: int = 0) -> dict:
     out = (C.c_double * 4)()
     _check(_lib.tv_last_frame_timing(int(device), out))
     return dict(start_ms=out[0], trace_ms=out[1], accum_ms=out[2], launches=int(out[3]))
+
+
+def diag_gather_ceiling(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, reps: int = 3) -> dict:
+    """Memory-latency ceiling of the trace kernel on this frame (include/tetvol_b200_diag.h):
+    the recorded tet-step sequences of every path replayed as dependent 64-B record loads."""
+    cam, rc = camera._c(), cfg._c()
+    out = (C.c_double * 6)()
+    _check(_lib.tv_diag_gather_ceiling(grid.handle, C.byref(cam), C.byref(rc), int(reps), out))
+    return dict(steps_per_s=out[0], steps_per_s_full_occupancy=out[1], steps=int(out[2]), replay_ms=out[3],
+                seq_bytes_per_step=out[4], warps_per_sm=int(out[5]))
+
+
+def ipc_export(dev_ptr: int) -> bytes:
+    """64-byte handle of a device allocation, for tv_ipc_open in another process."""
+    h = (C.c_uint8 * 64)()
+    _check(_lib.tv_ipc_export(C.c_void_p(dev_ptr), h))
+    return bytes(h)
+
+
+def ipc_open(handle: bytes, device: int = 0) -> int:
+    """Maps a peer process's allocation (tv_ipc_export) on `device`; returns the device pointer."""
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    out = C.c_void_p()
+    _check(_lib.tv_ipc_open(h, int(device), C.byref(out)))
+    return int(out.value)
+
+
+def ipc_close(dev_ptr: int) -> None:
+    _check(_lib.tv_ipc_close(C.c_void_p(dev_ptr)))
 
 
 def tile_pack_words(width: int, height: int, rank: int, n_ranks: int, elem_words: int) -> int:

@@ -22,6 +22,7 @@
 // index order, each decision / payload is certified against a rounding-error
 // bound and replayed sequentially in index order when the bound is ambiguous.
 #include <cub/cub.cuh>
+#include <cuda.h>
 
 #include <algorithm>
 #include <chrono>
@@ -29,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "tv_leb.cuh"
@@ -202,62 +204,11 @@ __device__ __forceinline__ float unord_f(uint32_t u) {
 
 __device__ __forceinline__ d3 corner(const uint4* verts, uint32_t v) { return vpos(verts[v]); }
 
-// descent step at an internal tet (tet_grid.cpp:453-470) using its NodeRec
-__device__ __forceinline__ uint32_t descend_owner(const NodeRec* split, const tv_tet* tets, uint32_t cur, d3 p) {
-    while (tets[cur].children[0] != kNone) {
-        const NodeRec& nd = split[cur];
-        const double sp = dot(mk(nd.n[0], nd.n[1], nd.n[2]), sub(p, mk(nd.pm[0], nd.pm[1], nd.pm[2])));
-        const bool take_a = nd.sref_pos ? (sp >= 0.0) : (sp <= 0.0);
-        cur = take_a ? nd.child[0] : nd.child[1];
-    }
-    return cur;
-}
-
 struct RootScan {
     uint32_t id[24];
     uint32_t nid[24];
     uint32_t vid[24][4];
 };
-
-// root scan (tet_grid.cpp:435-451) for every voxel centre
-__global__ void owner_init_kernel(RootScan R, const uint4* verts, int nx, int ny, int nz, uint32_t* owner) {
-    const uint64_t n = static_cast<uint64_t>(nx) * ny * nz;
-    for (uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; idx < n;
-         idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(idx % nx), j = static_cast<int>((idx / nx) % ny),
-                  k = static_cast<int>(idx / (static_cast<uint64_t>(nx) * ny));
-        const d3 p = mk((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz);
-        uint32_t cur = kNone;
-        double best = __longlong_as_double(0x7ff0000000000000ll);
-        for (int r = 0; r < 24; ++r) {
-            double worst = 0.0;
-            for (int slot = 0; slot < 4; ++slot) {
-                const uint32_t id = (R.nid[r] >> (8 * slot)) & 0xffu;
-                const d3 w = sub(p, vpos(verts[R.vid[r][(slot + 1) & 3]]));
-                worst = dmax(worst, ndot(id, w.x, w.y, w.z));
-            }
-            if (worst <= 1e-12) {
-                cur = R.id[r];
-                break;
-            }
-            if (worst < best) best = worst, cur = R.id[r];
-        }
-        owner[idx] = cur;
-    }
-}
-
-__global__ void owner_descend_kernel(const NodeRec* split, const tv_tet* tets, int nx, int ny, int nz,
-                                     uint32_t* owner) {
-    const uint64_t n = static_cast<uint64_t>(nx) * ny * nz;
-    for (uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; idx < n;
-         idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t o = owner[idx];
-        if (tets[o].children[0] == kNone) continue;
-        const int i = static_cast<int>(idx % nx), j = static_cast<int>((idx / nx) % ny),
-                  k = static_cast<int>(idx / (static_cast<uint64_t>(nx) * ny));
-        owner[idx] = descend_owner(split, tets, o, mk((i + 0.5) / nx, (j + 0.5) / ny, (k + 0.5) / nz));
-    }
-}
 
 __global__ void stats_zero_kernel(const uint32_t* list, uint32_t n, Stats* st, uint8_t* flags) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -273,10 +224,41 @@ __global__ void stats_zero_kernel(const uint32_t* list, uint32_t n, Stats* st, u
     flags[t] |= F_EVAL;
 }
 
-constexpr int kRun = 16;  // voxels per thread along x
+// ----------------------------------------------------- voxel ownership pass
+// One pass over the volume per round (replaces a separate owner-map descent and
+// a full-volume statistics pass). Mode kVoxInit (round 0): every voxel gets its
+// root (tet_grid.cpp:435-451) and adds to that root's statistics. Mode
+// kVoxDescend (later rounds): a voxel whose owner is still a leaf is skipped
+// without reading its density (its leaf was evaluated in an earlier round and
+// its ownership is final); every other voxel's owner was bisected in the last
+// closure, so it descends to its new leaf (tet_grid.cpp:453-470), which is
+// fresh, and adds to that leaf's statistics. Mode kVoxAll: every voxel adds to
+// its (final) owner, with the temperature / albedo channels (payload pass).
+//
+// Accumulation: each lane aggregates its voxels in registers while their owner
+// stays the same and adds the aggregate to the owner's statistics (global
+// fire-and-forget atomics) when the owner changes; at the end of a warp's chunk
+// all lanes flush warp-synchronously (one warp reduction and one atomic set
+// when the whole warp agrees on the owner, as it does while the tets are
+// large). The order of the double sums is free: every decision taken from
+// them is certified against a rounding bound (err_bound) or replayed
+// sequentially in voxel-index order.
+enum : int { kVoxInit = 0, kVoxDescend = 1, kVoxAll = 2 };
+constexpr int kVoxThreads = 256;
 
-__device__ __forceinline__ void flush(Stats* st, uint32_t L, const Stats& a, bool with_tl) {
-    Stats& s = st[L];
+struct Agg {
+    double sum, asum, tsum, tasum, lsum, lasum;
+    uint32_t cnt, mn, mx;
+};
+
+__device__ __forceinline__ void agg_reset(Agg& a) {
+    a.sum = a.asum = a.tsum = a.tasum = a.lsum = a.lasum = 0.0;
+    a.cnt = 0;
+    a.mn = 0xffffffffu;
+    a.mx = 0u;
+}
+
+__device__ __forceinline__ void stats_atomic(Stats& s, const Agg& a, bool with_tl) {
     atomicAdd(&s.sum, a.sum);
     atomicAdd(&s.asum, a.asum);
     atomicAdd(&s.cnt, a.cnt);
@@ -290,50 +272,203 @@ __device__ __forceinline__ void flush(Stats* st, uint32_t L, const Stats& a, boo
     }
 }
 
-// Per-voxel accumulation of (count, min, max, sum, |sum|) into the owner leaf,
-// for leaves flagged F_EVAL. Each thread walks a run of kRun voxels along x and
-// flushes with atomics only when the owner changes.
-__global__ void stats_accum_kernel(VolView V, const uint32_t* owner, const uint8_t* flags, Stats* st, int with_tl) {
-    const uint64_t runs_x = (V.nx + kRun - 1) / kRun;
-    const uint64_t n = runs_x * V.ny * V.nz;
-    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
-         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t row = r / runs_x;
-        const int i0 = static_cast<int>((r % runs_x) * kRun);
-        const uint64_t base = row * V.nx;
-        uint32_t cur = kNone;
-        Stats a{};
-        for (int i = i0; i < min(i0 + kRun, V.nx); ++i) {
-            const uint64_t idx = base + i;
-            const uint32_t L = owner[idx];
-            if (L != cur) {
-                if (cur != kNone && (flags[cur] & F_EVAL)) flush(st, cur, a, with_tl);
-                cur = L;
-                a.sum = a.asum = a.tsum = a.tasum = a.lsum = a.lasum = 0.0;
-                a.cnt = 0;
-                a.mn = 0xffffffffu;
-                a.mx = 0;
-            }
-            const float x = V.dens[idx];
-            a.sum += static_cast<double>(x);
-            a.asum += fabs(static_cast<double>(x));
-            a.cnt += 1;
-            a.mn = min(a.mn, ord_f(x));
-            a.mx = max(a.mx, ord_f(x));
-            if (with_tl) {
-                if (V.temp) {
-                    const double t = V.temp[idx];
-                    a.tsum += t;
-                    a.tasum += fabs(t);
-                }
-                if (V.alb) {
-                    const double l = V.alb[idx];
-                    a.lsum += l;
-                    a.lasum += fabs(l);
-                }
-            }
+// global fire-and-forget atomics (RED; f64 adds are native in L2, where
+// shared-memory f64 adds would be CAS loops)
+__device__ __forceinline__ void stats_atomic_at(Stats* st, uint32_t owner, const Agg& a, bool with_tl) {
+    stats_atomic(st[owner], a, with_tl);
+}
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// warp-synchronous flush of every lane's (cur, a) with has = a.cnt > 0
+__device__ __forceinline__ void warp_flush(Stats* st, uint32_t cur, Agg& a, bool with_tl) {
+    const bool has = a.cnt > 0;
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (!m) return;
+    const uint32_t c0 = __shfl_sync(0xffffffffu, cur, __ffs(m) - 1);
+    if (__all_sync(0xffffffffu, !has || cur == c0)) {
+        Agg r;
+        r.sum = wsum(a.sum);
+        r.asum = wsum(a.asum);
+        if (with_tl) {
+            r.tsum = wsum(a.tsum);
+            r.tasum = wsum(a.tasum);
+            r.lsum = wsum(a.lsum);
+            r.lasum = wsum(a.lasum);
         }
-        if (cur != kNone && (flags[cur] & F_EVAL)) flush(st, cur, a, with_tl);
+        uint32_t cnt = a.cnt, mn = a.mn, mx = a.mx;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        r.cnt = cnt, r.mn = mn, r.mx = mx;
+        if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(m) - 1)) stats_atomic_at(st, c0, r, with_tl);
+    } else if (has) {
+        stats_atomic_at(st, cur, a, with_tl);
+    }
+    agg_reset(a);
+}
+
+// root of voxel centre p (tet_grid.cpp:435-451): the root whose pyramid and
+// face triangle hold p, accepted with a 1e-9 interior margin (every other root
+// is then violated far beyond the scan's 1e-12), else the reference's scan
+__device__ __forceinline__ uint32_t root_of(const RootScan& R, const uint4* verts, d3 p) {
+    const int g = guess_root(p);
+    double worst = -__longlong_as_double(0x7ff0000000000000ll);
+    for (int slot = 0; slot < 4; ++slot) {
+        const uint32_t id = (R.nid[g] >> (8 * slot)) & 0xffu;
+        const d3 w = sub(p, vpos(verts[R.vid[g][(slot + 1) & 3]]));
+        worst = dmax(worst, ndot(id, w.x, w.y, w.z));
+    }
+    if (worst <= -1e-9) return R.id[g];
+    uint32_t o = kNone;
+    double best = __longlong_as_double(0x7ff0000000000000ll);
+    for (int rr = 0; rr < 24; ++rr) {
+        double wv = 0.0;
+        for (int slot = 0; slot < 4; ++slot) {
+            const uint32_t id = (R.nid[rr] >> (8 * slot)) & 0xffu;
+            const d3 w = sub(p, vpos(verts[R.vid[rr][(slot + 1) & 3]]));
+            wv = dmax(wv, ndot(id, w.x, w.y, w.z));
+        }
+        if (wv <= 1e-12) return R.id[rr];
+        if (wv < best) best = wv, o = R.id[rr];
+    }
+    return o;
+}
+
+__device__ __forceinline__ d3 voxel_centre(const VolView& V, uint64_t idx) {
+    const uint64_t row = idx / V.nx;
+    const int i = static_cast<int>(idx - row * V.nx), j = static_cast<int>(row % V.ny),
+              k = static_cast<int>(row / V.ny);
+    return mk((i + 0.5) / V.nx, (j + 0.5) / V.ny, (k + 0.5) / V.nz);  // volume.hpp:44-46
+}
+
+// descent from a bisected owner to the leaf holding p (tet_grid.cpp:453-470)
+__device__ __forceinline__ uint32_t descend(const NodeRec* split, const uint8_t* flags, uint32_t o, d3 p) {
+    do {
+        const NodeRec& nd = split[o];
+        const double sp = dot(mk(nd.n[0], nd.n[1], nd.n[2]), sub(p, mk(nd.pm[0], nd.pm[1], nd.pm[2])));
+        const bool take_a = nd.sref_pos ? (sp >= 0.0) : (sp <= 0.0);
+        o = take_a ? nd.child[0] : nd.child[1];
+    } while (!(flags[o] & F_LEAF));
+    return o;
+}
+
+// Sweep order: the volume is read as a flat array in groups of four voxels
+// (one 16-B owner load, one 16-B density load); lane l of a warp takes the
+// kVoxLaneGroups consecutive groups starting at group kVoxLaneGroups * l of
+// the warp's chunk, so a lane's voxels are contiguous (its owner changes only
+// at tet boundaries) and the warp's chunk is one contiguous span.
+constexpr int kVoxLaneGroups = 4;  // 16 voxels per lane, 512 per warp chunk
+
+struct VoxLane {
+    uint32_t cur = kNone;
+    Agg a;
+};
+
+__device__ __forceinline__ void vox_add(Stats* st, VoxLane& L, uint32_t o, float x, const VolView& V,
+                                        uint64_t idx, bool with_tl) {
+    if (o != L.cur) {
+        if (L.a.cnt) stats_atomic_at(st, L.cur, L.a, with_tl);
+        agg_reset(L.a);
+        L.cur = o;
+    }
+    L.a.sum += static_cast<double>(x);
+    L.a.asum += fabs(static_cast<double>(x));
+    L.a.cnt += 1;
+    L.a.mn = min(L.a.mn, ord_f(x));
+    L.a.mx = max(L.a.mx, ord_f(x));
+    if (with_tl) {
+        if (V.temp) {
+            const double tv = V.temp[idx];
+            L.a.tsum += tv;
+            L.a.tasum += fabs(tv);
+        }
+        if (V.alb) {
+            const double lv = V.alb[idx];
+            L.a.lsum += lv;
+            L.a.lasum += fabs(lv);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kVoxThreads) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
+                                                                 const NodeRec* split, const uint8_t* flags,
+                                                                 uint32_t* owner, Stats* st, int mode, int with_tl) {
+    const uint64_t nvox = static_cast<uint64_t>(V.nx) * V.ny * V.nz;
+    const uint64_t n4 = nvox / 4;
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t n_warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    const uint64_t per_warp = 32ull * kVoxLaneGroups;
+    uint4* own4 = reinterpret_cast<uint4*>(owner);
+    const float4* d4p = reinterpret_cast<const float4*>(V.dens);
+    for (uint64_t c = warp * per_warp; c < n4; c += n_warps * per_warp) {
+        VoxLane L;
+        agg_reset(L.a);
+#pragma unroll 1
+        for (int q = 0; q < kVoxLaneGroups; ++q) {
+            const uint64_t g = c + static_cast<uint64_t>(lane) * kVoxLaneGroups + q;
+            if (g >= n4) break;
+            const uint64_t idx0 = 4 * g;
+            uint4 o4;
+            if (mode == kVoxInit) {
+                o4.x = root_of(R, verts, voxel_centre(V, idx0));
+                o4.y = root_of(R, verts, voxel_centre(V, idx0 + 1));
+                o4.z = root_of(R, verts, voxel_centre(V, idx0 + 2));
+                o4.w = root_of(R, verts, voxel_centre(V, idx0 + 3));
+                own4[g] = o4;
+            } else {
+                o4 = own4[g];
+                if (mode == kVoxDescend) {
+                    // voxels whose owner is still a leaf keep it and were counted
+                    // when it was evaluated: skip them (no density read)
+                    const bool l0 = flags[o4.x] & F_LEAF, l1 = flags[o4.y] & F_LEAF, l2 = flags[o4.z] & F_LEAF,
+                               l3 = flags[o4.w] & F_LEAF;
+                    if (l0 & l1 & l2 & l3) continue;
+                    const float4 d4 = d4p[g];
+                    if (!l0) vox_add(st, L, o4.x = descend(split, flags, o4.x, voxel_centre(V, idx0)), d4.x, V,
+                                     idx0, with_tl);
+                    if (!l1) vox_add(st, L, o4.y = descend(split, flags, o4.y, voxel_centre(V, idx0 + 1)), d4.y,
+                                     V, idx0 + 1, with_tl);
+                    if (!l2) vox_add(st, L, o4.z = descend(split, flags, o4.z, voxel_centre(V, idx0 + 2)), d4.z,
+                                     V, idx0 + 2, with_tl);
+                    if (!l3) vox_add(st, L, o4.w = descend(split, flags, o4.w, voxel_centre(V, idx0 + 3)), d4.w,
+                                     V, idx0 + 3, with_tl);
+                    own4[g] = o4;
+                    continue;
+                }
+            }
+            const float4 d4 = d4p[g];
+            vox_add(st, L, o4.x, d4.x, V, idx0, with_tl);
+            vox_add(st, L, o4.y, d4.y, V, idx0 + 1, with_tl);
+            vox_add(st, L, o4.z, d4.z, V, idx0 + 2, with_tl);
+            vox_add(st, L, o4.w, d4.w, V, idx0 + 3, with_tl);
+        }
+        warp_flush(st, L.cur, L.a, with_tl);
+    }
+    // the last nvox % 4 voxels, scalar
+    if (blockIdx.x == 0 && threadIdx.x < nvox - 4 * n4) {
+        const uint64_t idx = 4 * n4 + threadIdx.x;
+        uint32_t o = mode == kVoxInit ? root_of(R, verts, voxel_centre(V, idx)) : owner[idx];
+        bool add = true;
+        if (mode == kVoxDescend) {
+            if (flags[o] & F_LEAF) add = false;
+            else o = descend(split, flags, o, voxel_centre(V, idx));
+        }
+        if (mode != kVoxAll) owner[idx] = o;
+        if (add) {
+            VoxLane L;
+            agg_reset(L.a);
+            vox_add(st, L, o, V.dens[idx], V, idx, with_tl);
+            stats_atomic_at(st, L.cur, L.a, with_tl);
+        }
     }
 }
 
@@ -540,9 +675,9 @@ __global__ void dedup_assign_kernel(const uint64_t* hi, const uint32_t* lo, cons
 
 // tet_grid.cpp:339-382 for all marked leaves at once; children get ids
 // n_t + 2i, n_t + 2i + 1 in marked-list (ascending id) order.
-__global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, tv_tet* tets, const uint4* verts,
-                              const uint32_t* mid_vid, NodeRec* split, uint8_t* flags, uint8_t* vtouch, int max_level,
-                              int* err) {
+__global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, tv_tet* tets, uint4* tv4,
+                              const uint4* verts, const uint32_t* mid_vid, NodeRec* split, uint8_t* flags,
+                              uint8_t* vtouch, int max_level, int* err) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t t = marked[i];
@@ -550,7 +685,8 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
     if (parent.level >= max_level) atomicOr(err, E_LEVEL);  // MaxLevelExceeded (tet_grid.cpp:342)
     int s0, s1;
     refinement_slots(parent, verts, s0, s1);
-    const uint32_t vm = mid_vid[i];
+    uint32_t vm = mid_vid[i];
+    if (vm == kNone) vm = parent.verts[s0];  // midpoint error (already flagged): stay in bounds
     const uint32_t ida = n_t + 2 * i, idb = ida + 1;
     tv_tet a = parent, b = parent;
     a.verts[s1] = vm;
@@ -568,6 +704,8 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
     }
     tets[ida] = a;
     tets[idb] = b;
+    tv4[ida] = make_uint4(a.verts[0], a.verts[1], a.verts[2], a.verts[3]);
+    tv4[idb] = make_uint4(b.verts[0], b.verts[1], b.verts[2], b.verts[3]);
     tets[t].children[0] = ida;
     tets[t].children[1] = idb;
     tets[t].neighbors[0] = tets[t].neighbors[1] = tets[t].neighbors[2] = tets[t].neighbors[3] = kNone;
@@ -597,22 +735,21 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
     split[t] = r;
 }
 
-// mark leaves with a hanging edge; only leaves that are new or have >= 2
-// vertices touched by the last bisect pass can have one
-__global__ void hanging_kernel(const uint32_t* leaves, uint32_t n, const tv_tet* tets, const uint4* verts,
-                               const uint32_t* table, uint64_t mask, const uint8_t* vtouch, uint8_t* flags,
-                               uint32_t* n_marked) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t t = leaves[i];
-    const tv_tet tt = tets[t];
+// Mark every leaf with a hanging edge (an edge whose integer midpoint is a
+// vertex), over all tet ids. Only two kinds of leaf can have one: the children
+// made by the last bisect pass (ids >= first_new) and older leaves with at
+// least two vertices touched by that pass (a new midpoint lies on an edge of the
+// bisected tet, whose two endpoints were touched).
+__global__ void hanging_kernel(uint32_t n_t, uint32_t first_new, const uint4* __restrict__ tv4,
+                               const uint4* __restrict__ verts, const uint32_t* __restrict__ table, uint64_t mask,
+                               const uint8_t* __restrict__ vtouch, uint8_t* flags) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_t) return;
     const uint8_t f = flags[t];
-    if (!(f & F_NEW)) {
-        const int touched = vtouch[tt.verts[0]] + vtouch[tt.verts[1]] + vtouch[tt.verts[2]] + vtouch[tt.verts[3]];
-        if (touched < 2) return;
-    }
-    uint4 q[4];
-    for (int k = 0; k < 4; ++k) q[k] = verts[tt.verts[k]];
+    if (!(f & F_LEAF)) return;
+    const uint4 tv = tv4[t];
+    if (t < first_new && vtouch[tv.x] + vtouch[tv.y] + vtouch[tv.z] + vtouch[tv.w] < 2) return;
+    uint4 q[4] = {verts[tv.x], verts[tv.y], verts[tv.z], verts[tv.w]};
     for (int e = 0; e < 6; ++e) {
         const uint4 a = q[ep0(e)], b = q[ep1(e)];
         const uint64_t sx = static_cast<uint64_t>(a.x) + b.x, sy = static_cast<uint64_t>(a.y) + b.y,
@@ -621,16 +758,27 @@ __global__ void hanging_kernel(const uint32_t* leaves, uint32_t n, const tv_tet*
         if (hash_find(table, mask, verts, static_cast<uint32_t>(sx / 2), static_cast<uint32_t>(sy / 2),
                       static_cast<uint32_t>(sz / 2)) != kNone) {
             flags[t] = f | F_MARK;
-            atomicAdd(n_marked, 1u);
             return;
         }
     }
 }
 
-__global__ void flag_select_kernel(const uint8_t* flags, uint32_t n, uint8_t bit, uint8_t* out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = (flags[i] & bit) ? 1 : 0;
+// tet ids whose flag has `bit` set, for cub::DeviceSelect::If over ids
+struct FlagBit {
+    const uint8_t* flags;
+    uint8_t bit;
+    __device__ __forceinline__ bool operator()(uint32_t t) const { return flags[t] & bit; }
+};
+
+// the end-of-pass counters the host reads in one copy: [0] vertices added by
+// the pass, [1] leaves marked for the next pass, [2] error bits
+__global__ void pass_state_kernel(const uint32_t* scan, uint32_t n_miss, const uint32_t* n_marked, const int* err,
+                                  uint32_t* out) {
+    out[0] = n_miss ? scan[n_miss - 1] : 0u;
+    out[1] = *n_marked;
+    out[2] = static_cast<uint32_t>(*err);
 }
+
 __global__ void list_flag_kernel(const uint32_t* list, uint32_t n, const uint8_t* flags, uint8_t bit, uint8_t* out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = (flags[list[i]] & bit) ? 1 : 0;
@@ -639,11 +787,6 @@ __global__ void clear_flag_kernel(const uint32_t* list, uint32_t n, uint8_t* fla
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) flags[list[i]] &= static_cast<uint8_t>(~bit);
 }
-__global__ void iota_kernel(uint32_t* out, uint32_t n) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = i;
-}
-
 struct PayloadParams {
     double scale;
     int has_t, has_a;
@@ -785,13 +928,83 @@ __global__ void gather_face_hi_kernel(const uint32_t* rec, uint64_t n, const uin
 // ------------------------------------------------------------ host side
 inline unsigned nblk(uint64_t n, unsigned t = 256) { return static_cast<unsigned>(std::max<uint64_t>((n + t - 1) / t, 1)); }
 
-// Build scratch comes from the device's stream-ordered memory pool (kept
-// cached across builds, see build_grid), not from cudaMalloc / cudaFree.
+// Build scratch: growable device arrays. Each buffer reserves a virtual
+// address range once and maps physical memory onto its end as it grows
+// (cuMemCreate / cuMemMap, reached through the runtime's driver entry points so
+// the library does not link libcuda): growth copies nothing and never holds
+// the old and new copies at once, and mapping costs ~1 ms per GB where a
+// stream-ordered pool's first growth costs 65-100 ms per GB
+// (tools/alloc_probe.cu on B200). Everything is unmapped when the buffer goes
+// out of scope, so no build scratch outlives the build. Without the VMM entry
+// points, buffers fall back to cudaMalloc + copy on growth.
+struct VmmApi {
+    using Create = CUresult (*)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    using Release = CUresult (*)(CUmemGenericAllocationHandle);
+    using Reserve = CUresult (*)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    using AddrFree = CUresult (*)(CUdeviceptr, size_t);
+    using Map = CUresult (*)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    using Unmap = CUresult (*)(CUdeviceptr, size_t);
+    using Access = CUresult (*)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    using Gran = CUresult (*)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+    Create create = nullptr;
+    Release release = nullptr;
+    Reserve reserve = nullptr;
+    AddrFree addr_free = nullptr;
+    Map map = nullptr;
+    Unmap unmap = nullptr;
+    Access access = nullptr;
+    Gran gran = nullptr;
+    bool ok = false;
+};
+
+const VmmApi& vmm() {
+    static VmmApi api = [] {
+        VmmApi a;
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn;
+        };
+        a.ok = get("cuMemCreate", reinterpret_cast<void**>(&a.create)) &&
+               get("cuMemRelease", reinterpret_cast<void**>(&a.release)) &&
+               get("cuMemAddressReserve", reinterpret_cast<void**>(&a.reserve)) &&
+               get("cuMemAddressFree", reinterpret_cast<void**>(&a.addr_free)) &&
+               get("cuMemMap", reinterpret_cast<void**>(&a.map)) &&
+               get("cuMemUnmap", reinterpret_cast<void**>(&a.unmap)) &&
+               get("cuMemSetAccess", reinterpret_cast<void**>(&a.access)) &&
+               get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&a.gran));
+        if (std::getenv("TV_BUILD_NO_VMM")) a.ok = false;
+        return a;
+    }();
+    return api;
+}
+
+thread_local int t_build_device = 0;
+
 struct Buf {
     void* p = nullptr;
-    size_t bytes = 0;
-    ~Buf() {
-        if (p) cudaFreeAsync(p, 0);
+    size_t bytes = 0;  // usable (mapped) bytes
+    CUdeviceptr va = 0;
+    size_t reserved = 0;
+    std::vector<CUmemGenericAllocationHandle> handles;
+    bool mapped = false;  // VMM-backed
+    Buf() = default;
+    Buf(const Buf&) = delete;
+    Buf& operator=(const Buf&) = delete;
+    ~Buf() { reset(); }
+    void reset() {
+        if (!p) return;
+        cudaStreamSynchronize(0);  // build kernels run on the legacy stream
+        if (mapped) {
+            const VmmApi& a = vmm();
+            a.unmap(va, bytes);
+            for (auto h : handles) a.release(h);
+            a.addr_free(va, reserved);
+        } else {
+            cudaFree(p);
+        }
+        p = nullptr, bytes = 0, va = 0, reserved = 0, mapped = false;
+        handles.clear();
     }
     template <class T>
     T* as() {
@@ -799,39 +1012,70 @@ struct Buf {
     }
 };
 
-int ensure(Buf& b, size_t bytes, bool keep = false) {
+// grow b to at least `bytes`, keeping its contents
+int ensure(Buf& b, size_t bytes, bool /*keep: contents are always kept*/ = false) {
     if (b.bytes >= bytes) return TV_OK;
-    const size_t nb = std::max(bytes, 2 * b.bytes);  // doubling: each pool growth maps GBs (10-300 ms)
     static const bool verbose = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
-    const bool log = verbose && nb >= (256u << 20);
-    auto t0 = std::chrono::steady_clock::now();
-    auto lap = [&]() {
-        cudaDeviceSynchronize();
-        const auto t = std::chrono::steady_clock::now();
-        const double ms = std::chrono::duration<double, std::milli>(t - t0).count();
-        t0 = t;
-        return ms;
-    };
-    if (log) lap();
-    void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, nb, 0);
-    if (e != cudaSuccess) return cuda_status(e, "build alloc");
-    const double ms_alloc = log ? lap() : 0.0;
-    if (keep && b.p && b.bytes) {
-        e = cudaMemcpyAsync(p, b.p, b.bytes, cudaMemcpyDeviceToDevice, 0);
-        if (e != cudaSuccess) {
-            cudaFreeAsync(p, 0);
-            return cuda_status(e, "build grow");
+    const auto t0 = std::chrono::steady_clock::now();
+    const VmmApi& a = vmm();
+    // geometric growth in >= 64 MB steps: few mappings per buffer
+    size_t nb = std::max(bytes, 2 * b.bytes);
+    if (a.ok && (b.mapped || !b.p)) {
+        CUmemAllocationProp prop = {};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = t_build_device;
+        size_t g = 0;
+        if (a.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !g) g = 2u << 20;
+        nb = std::max(nb, static_cast<size_t>(64u << 20));
+        nb = (nb + g - 1) / g * g;
+        if (!b.va) {
+            size_t total = 0, free_b = 0;
+            cudaMemGetInfo(&free_b, &total);
+            b.reserved = (std::max(total, nb) + g - 1) / g * g;  // virtual only
+            if (a.reserve(&b.va, b.reserved, g, 0, 0) != CUDA_SUCCESS)
+                return set_error(TV_ERR_OOM, "build alloc: cannot reserve a virtual range");
+            b.p = reinterpret_cast<void*>(b.va);
+            b.mapped = true;
         }
+        if (nb > b.reserved) return set_error(TV_ERR_OOM, "build alloc: buffer exceeds device memory");
+        const size_t add = nb - b.bytes;
+        CUmemGenericAllocationHandle h;
+        if (a.create(&h, add, &prop, 0) != CUDA_SUCCESS)
+            return set_error(TV_ERR_OOM, "build alloc: out of device memory");
+        if (a.map(b.va + b.bytes, add, 0, h, 0) != CUDA_SUCCESS) {
+            a.release(h);
+            return set_error(TV_ERR_OOM, "build alloc: map failed");
+        }
+        CUmemAccessDesc d = {};
+        d.location = prop.location;
+        d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (a.access(b.va + b.bytes, add, &d, 1) != CUDA_SUCCESS) {
+            a.unmap(b.va + b.bytes, add);
+            a.release(h);
+            return set_error(TV_ERR_OOM, "build alloc: access failed");
+        }
+        b.handles.push_back(h);
+        b.bytes = nb;
+    } else {
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e != cudaSuccess) return cuda_status(e, "build alloc");
+        if (b.p && b.bytes) {
+            e = cudaMemcpy(p, b.p, b.bytes, cudaMemcpyDeviceToDevice);
+            if (e != cudaSuccess) {
+                cudaFree(p);
+                return cuda_status(e, "build grow");
+            }
+        }
+        b.reset();
+        b.p = p;
+        b.bytes = nb;
     }
-    const double ms_copy = log ? lap() : 0.0;
-    if (b.p) cudaFreeAsync(b.p, 0);
-    const double ms_free = log ? lap() : 0.0;
-    if (log)
-        std::fprintf(stderr, "tetvol_b200: build alloc %.1f MB: malloc %.2f copy %.2f free %.2f ms\n", nb / 1048576.0,
-                     ms_alloc, ms_copy, ms_free);
-    b.p = p;
-    b.bytes = nb;
+    if (verbose && nb >= (256u << 20))
+        std::fprintf(stderr, "tetvol_b200: build alloc %.1f MB (%s): %.2f ms\n", nb / 1048576.0,
+                     b.mapped ? "vmm" : "cudaMalloc",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     return TV_OK;
 }
 
@@ -892,19 +1136,14 @@ int validate_build_cfg(const tv_build_config* c) {  // builder.cpp:12-17
 // defined in tv_capi.cu
 int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]);
 
-int build_grid(const float* dens, const float* temp, const float* alb, int nx, int ny, int nz,
-               const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out, tv_build_stats* stats) {
+namespace {
+int build_grid_impl(const float* dens, const float* temp, const float* alb, int nx, int ny, int nz,
+                    const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out,
+                    tv_build_stats* stats) {
     int rc = validate_build_cfg(cfg);
     if (rc) return rc;
     if (cfg->use_camera && !camera) return set_error(TV_ERR_CONFIG, "useCamera set but no camera given");
     if (nx < 1 || ny < 1 || nz < 1) return set_error(TV_ERR_CONFIG, "volume dimensions must be positive");
-    {  // keep up to 32 GB of build scratch cached in the pool between builds
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t keep = 32ull << 30;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    }
     EvalParams E{};
     E.thr = cfg->variation_threshold;
     E.max_level = cfg->max_level;
@@ -927,9 +1166,8 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     cudaEventRecord(e0);
 
     const uint64_t nvox = static_cast<uint64_t>(nx) * ny * nz;
-    VolView V{dens, temp, alb, nx, ny, nz};
-    Buf tets_b, verts_b, split_b, flags_b, stats_b, table_b, vtouch_b, owner_b, list_b, list2_b, leaves_b, sel_b,
-        tmp_b, mid_b, miss_hi_b, miss_lo_b, miss_idx_b, miss_hi2_b, miss_lo2_b, miss_idx2_b, head_b, scan_b, misc_b;
+    Buf align_b[3];  // misaligned channels, copied (see below)
+    Buf tets_b, tv4_b, verts_b, split_b, flags_b, stats_b, table_b, vtouch_b, owner_b, leaves_b, sel_b, tmp_b, mid_b, miss_hi_b, miss_lo_b, miss_idx_b, miss_hi2_b, miss_lo2_b, miss_idx2_b, head_b, scan_b, misc_b;
     size_t cap_t = 0, cap_v = 0;
     uint64_t hmask = 0;
 
@@ -945,10 +1183,21 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     } while (0)
 #define CK(x, what) TRY(cuda_status((x), what))
 
+    // the voxel sweep reads the channels as float4: copy a misaligned one
+    const float* ch[3] = {dens, temp, alb};
+    for (int c = 0; c < 3; ++c)
+        if (ch[c] && (reinterpret_cast<uintptr_t>(ch[c]) & 15u)) {
+            TRY(ensure(align_b[c], nvox * sizeof(float)));
+            CK(cudaMemcpy(align_b[c].p, ch[c], nvox * sizeof(float), cudaMemcpyDeviceToDevice), "align volume");
+            ch[c] = align_b[c].as<float>();
+        }
+    const VolView V{ch[0], ch[1], ch[2], nx, ny, nz};
+
     auto grow_tets = [&](size_t need) -> int {
         if (need <= cap_t) return TV_OK;
         const size_t nc = std::max(need, cap_t * 2 + 1024);
         TRY(ensure(tets_b, nc * sizeof(tv_tet), true));
+        TRY(ensure(tv4_b, nc * sizeof(uint4), true));
         TRY(ensure(split_b, nc * sizeof(NodeRec), true));
         TRY(ensure(flags_b, nc, true));
         TRY(ensure(stats_b, nc * sizeof(Stats), true));
@@ -975,6 +1224,12 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     TRY(grow_tets(std::min<size_t>(std::max<size_t>(1 << 16, nvox / 4), size_t(1) << 24)));
     CK(cudaMemcpy(tets_b.p, ht.data(), ht.size() * sizeof(tv_tet), cudaMemcpyHostToDevice), "roots H2D");
     {
+        std::vector<uint4> tv(ht.size());
+        for (size_t i = 0; i < ht.size(); ++i)
+            tv[i] = make_uint4(ht[i].verts[0], ht[i].verts[1], ht[i].verts[2], ht[i].verts[3]);
+        CK(cudaMemcpy(tv4_b.p, tv.data(), tv.size() * sizeof(uint4), cudaMemcpyHostToDevice), "roots H2D");
+    }
+    {
         const size_t need_v = std::min<size_t>(std::max<size_t>(1 << 15, nvox / 16), size_t(1) << 22);
         TRY(ensure(verts_b, need_v * sizeof(uint4)));
         CK(cudaMemcpy(verts_b.p, hv.data(), hv.size() * sizeof(uint4), cudaMemcpyHostToDevice), "verts H2D");
@@ -991,6 +1246,7 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     uint32_t* d_cnt = reinterpret_cast<uint32_t*>(misc_b.as<char>() + 8);
     unsigned long long* d_ctr = reinterpret_cast<unsigned long long*>(misc_b.as<char>() + 16);  // replays, visits
     int* d_depth = reinterpret_cast<int*>(misc_b.as<char>() + 32);
+    uint32_t* d_state = reinterpret_cast<uint32_t*>(misc_b.as<char>() + 48);  // pass_state_kernel
     CK(cudaMemset(misc_b.p, 0, 64), "misc");
 
     RootScan R;
@@ -1001,35 +1257,40 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
                    static_cast<uint32_t>(t.normal_ids[3]) << 24;
         for (int k = 0; k < 4; ++k) R.vid[r][k] = t.verts[k];
     }
-    owner_init_kernel<<<148 * 8, 256>>>(R, verts_b.as<uint4>(), nx, ny, nz, owner_b.as<uint32_t>());
-    CK(cudaGetLastError(), "owner init");
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device);
+    const unsigned vox_blocks = static_cast<unsigned>(n_sm) * (2048 / kVoxThreads);
 
-    // device lists
-    auto select_flagged = [&](const uint32_t* in_list, uint32_t n_in, uint8_t bit, Buf& outb, uint32_t& n_out,
-                              bool from_all) -> int {
+    // the listed tets whose flag has `bit` (order kept)
+    auto select_listed = [&](const uint32_t* in_list, uint32_t n_in, uint8_t bit, Buf& outb, uint32_t& n_out) -> int {
         TRY(ensure(sel_b, std::max<size_t>(n_in, 1)));
         TRY(ensure(outb, std::max<size_t>(n_in, 1) * sizeof(uint32_t)));
-        if (from_all) {
-            flag_select_kernel<<<nblk(n_in), 256>>>(flags_b.as<uint8_t>(), n_in, bit, sel_b.as<uint8_t>());
-        } else {
-            list_flag_kernel<<<nblk(n_in), 256>>>(in_list, n_in, flags_b.as<uint8_t>(), bit, sel_b.as<uint8_t>());
-        }
+        list_flag_kernel<<<nblk(n_in), 256>>>(in_list, n_in, flags_b.as<uint8_t>(), bit, sel_b.as<uint8_t>());
         CK(cudaGetLastError(), "flag kernel");
-        const uint32_t* src = in_list;
-        if (from_all) {
-            TRY(ensure(list2_b, std::max<size_t>(n_in, 1) * sizeof(uint32_t)));
-            iota_kernel<<<nblk(n_in), 256>>>(list2_b.as<uint32_t>(), n_in);
-            src = list2_b.as<uint32_t>();
-        }
         size_t tb = 0;
-        CK(cub::DeviceSelect::Flagged(nullptr, tb, src, sel_b.as<uint8_t>(), outb.as<uint32_t>(), d_cnt,
+        CK(cub::DeviceSelect::Flagged(nullptr, tb, in_list, sel_b.as<uint8_t>(), outb.as<uint32_t>(), d_cnt,
                                       static_cast<int>(n_in)),
            "select sizing");
         TRY(ensure(tmp_b, tb));
-        CK(cub::DeviceSelect::Flagged(tmp_b.p, tb, src, sel_b.as<uint8_t>(), outb.as<uint32_t>(), d_cnt,
+        CK(cub::DeviceSelect::Flagged(tmp_b.p, tb, in_list, sel_b.as<uint8_t>(), outb.as<uint32_t>(), d_cnt,
                                       static_cast<int>(n_in)),
            "select");
         CK(cudaMemcpy(&n_out, d_cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost), "select count");
+        return TV_OK;
+    };
+    // all tet ids [0, n_t) whose flag has `bit`, ascending; the count lands in
+    // d_cnt and is copied to n_out when n_out is given
+    auto select_tets = [&](uint8_t bit, Buf& outb, uint32_t* n_out) -> int {
+        TRY(ensure(outb, std::max<size_t>(n_t, 1) * sizeof(uint32_t)));
+        cub::CountingInputIterator<uint32_t> ids(0);
+        const FlagBit pred{flags_b.as<uint8_t>(), bit};
+        size_t tb = 0;
+        CK(cub::DeviceSelect::If(nullptr, tb, ids, outb.as<uint32_t>(), d_cnt, static_cast<int>(n_t), pred),
+           "select sizing");
+        TRY(ensure(tmp_b, tb));
+        CK(cub::DeviceSelect::If(tmp_b.p, tb, ids, outb.as<uint32_t>(), d_cnt, static_cast<int>(n_t), pred),
+           "select");
+        if (n_out) CK(cudaMemcpy(n_out, d_cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost), "select count");
         return TV_OK;
     };
 
@@ -1063,20 +1324,20 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     for (;;) {
         const auto t_round = now();
         // ---- eval fresh leaves ----
-        if (rounds > 0) {
-            owner_descend_kernel<<<148 * 8, 256>>>(split_b.as<NodeRec>(), tets_b.as<tv_tet>(), nx, ny, nz,
-                                                   owner_b.as<uint32_t>());
-            CK(cudaGetLastError(), "owner descend");
-        }
         clear_flag_kernel<<<nblk(n_fresh), 256>>>(fresh_b.as<uint32_t>(), n_fresh, flags_b.as<uint8_t>(), F_NEW);
         stats_zero_kernel<<<nblk(n_fresh), 256>>>(fresh_b.as<uint32_t>(), n_fresh, stats_b.as<Stats>(),
                                                   flags_b.as<uint8_t>());
-        stats_accum_kernel<<<148 * 8, 256>>>(V, owner_b.as<uint32_t>(), flags_b.as<uint8_t>(), stats_b.as<Stats>(), 0);
+        // round 0: root scan of every voxel; later: descend the voxels whose
+        // owner was bisected, skip the rest
+        vox_stats_kernel<<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
+                                                      flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
+                                                      stats_b.as<Stats>(), rounds == 0 ? kVoxInit : kVoxDescend, 0);
+        CK(cudaGetLastError(), "voxel ownership");
         eval_kernel<<<nblk(n_fresh, 128), 128>>>(fresh_b.as<uint32_t>(), n_fresh, V, owner_b.as<uint32_t>(),
                                                   tets_b.as<tv_tet>(), verts_b.as<uint4>(), stats_b.as<Stats>(), E,
                                                   flags_b.as<uint8_t>(), d_ctr);
         CK(cudaGetLastError(), "eval");
-        TRY(select_flagged(fresh_b.as<uint32_t>(), n_fresh, F_MARK, marked_b, n_marked, false));
+        TRY(select_listed(fresh_b.as<uint32_t>(), n_fresh, F_MARK, marked_b, n_marked));
         const double ms_eval = verbose ? since(t_round) : 0.0;
         if (verbose) {
             unsigned long long c[2];
@@ -1147,38 +1408,39 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
                 CK(cub::DeviceScan::InclusiveSum(tmp_b.p, tb3, head_b.as<uint32_t>(), scan_b.as<uint32_t>(),
                                                  static_cast<int>(n_miss)),
                    "scan");
-                uint32_t n_new = 0;
-                CK(cudaMemcpy(&n_new, scan_b.as<uint32_t>() + n_miss - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost),
-                   "new verts");
-                TRY(grow_verts(static_cast<size_t>(n_v) + n_new));
+                // capacity for n_v + n_marked vertices is already mapped (n_new <= n_miss)
                 dedup_assign_kernel<<<nblk(n_miss), 256>>>(miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>(),
                                                            miss_idx_b.as<uint32_t>(), head_b.as<uint32_t>(),
                                                            scan_b.as<uint32_t>(), n_miss, n_v, verts_b.as<uint4>(),
                                                            table_b.as<uint32_t>(), hmask, mid_b.as<uint32_t>());
                 CK(cudaGetLastError(), "dedup assign");
-                n_v += n_new;
             }
             if (verbose) ph[0] += since(tp), tp = now();
-            CK(cudaMemset(vtouch_b.p, 0, n_v), "vtouch");
+            CK(cudaMemset(vtouch_b.p, 0, n_v), "vtouch");  // bisect touches existing vertices only
             bisect_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, n_t, tets_b.as<tv_tet>(),
-                                                   verts_b.as<uint4>(), mid_b.as<uint32_t>(), split_b.as<NodeRec>(),
-                                                   flags_b.as<uint8_t>(), vtouch_b.as<uint8_t>(), grid_max_level, d_err);
+                                                   tv4_b.as<uint4>(), verts_b.as<uint4>(), mid_b.as<uint32_t>(),
+                                                   split_b.as<NodeRec>(), flags_b.as<uint8_t>(),
+                                                   vtouch_b.as<uint8_t>(), grid_max_level, d_err);
             CK(cudaGetLastError(), "bisect");
+            const uint32_t first_new = n_t;
             n_t += 2 * n_marked;
             bisections += n_marked;
             ++passes;
-            CK(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost), "err");
-            if (herr) break;
             if (verbose) ph[1] += since(tp), tp = now();
-            // leaf list, hanging test
-            TRY(select_flagged(nullptr, n_t, F_LEAF, leaves_b, n_leaves, true));
-            CK(cudaMemset(d_cnt, 0, sizeof(uint32_t)), "memset");
-            hanging_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, tets_b.as<tv_tet>(),
-                                                    verts_b.as<uint4>(), table_b.as<uint32_t>(), hmask,
-                                                    vtouch_b.as<uint8_t>(), flags_b.as<uint8_t>(), d_cnt);
+            // hanging test over every tet id, then the marked list (ascending ids)
+            hanging_kernel<<<nblk(n_t), 256>>>(n_t, first_new, tv4_b.as<uint4>(), verts_b.as<uint4>(),
+                                               table_b.as<uint32_t>(), hmask, vtouch_b.as<uint8_t>(),
+                                               flags_b.as<uint8_t>());
             CK(cudaGetLastError(), "hanging");
             if (verbose) ph[2] += since(tp), tp = now();
-            TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_MARK, marked_b, n_marked, false));
+            TRY(select_tets(F_MARK, marked_b, nullptr));
+            pass_state_kernel<<<1, 1>>>(scan_b.as<uint32_t>(), n_miss, d_cnt, d_err, d_state);
+            uint32_t hs[3];
+            CK(cudaMemcpy(hs, d_state, sizeof(hs), cudaMemcpyDeviceToHost), "pass state");
+            n_v += hs[0];
+            n_marked = hs[1];
+            herr = static_cast<int>(hs[2]);
+            if (herr) break;
             clear_flag_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, flags_b.as<uint8_t>(), F_MARK);
             CK(cudaGetLastError(), "clear");
             if (verbose) ph[3] += since(tp);
@@ -1188,7 +1450,7 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
                          rounds, ph[0], ph[1], ph[2], ph[3]);
         if (herr) break;
         // fresh = leaves created in this round
-        TRY(select_flagged(leaves_b.as<uint32_t>(), n_leaves, F_NEW, fresh_b, n_fresh, false));
+        TRY(select_tets(F_NEW, fresh_b, &n_fresh));
         if (verbose) std::fprintf(stderr, "tetvol_b200: build round %d: closure done, %.2f ms total\n", rounds,
                                   since(t_round));
         mark();
@@ -1201,12 +1463,18 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     }
 
     // ---- payloads for every leaf (builder.cpp:164-182) ----
-    TRY(select_flagged(nullptr, n_t, F_LEAF, leaves_b, n_leaves, true));
-    owner_descend_kernel<<<148 * 8, 256>>>(split_b.as<NodeRec>(), tets_b.as<tv_tet>(), nx, ny, nz,
-                                           owner_b.as<uint32_t>());
-    stats_zero_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, stats_b.as<Stats>(),
-                                               flags_b.as<uint8_t>());
-    stats_accum_kernel<<<148 * 8, 256>>>(V, owner_b.as<uint32_t>(), flags_b.as<uint8_t>(), stats_b.as<Stats>(), 1);
+    TRY(select_tets(F_LEAF, leaves_b, &n_leaves));
+    // Every leaf's density statistics are those of its evaluation round (its
+    // voxels have not changed owner since). Temperature / albedo sums need one
+    // more pass over the (final) owner map.
+    if (temp || alb) {
+        stats_zero_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, stats_b.as<Stats>(),
+                                                   flags_b.as<uint8_t>());
+        vox_stats_kernel<<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
+                                                      flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
+                                                      stats_b.as<Stats>(), kVoxAll, 1);
+        CK(cudaGetLastError(), "voxel statistics");
+    }
     PayloadParams PP{cfg->density_scale, temp != nullptr, alb != nullptr};
     payload_kernel<<<nblk(n_leaves, 128), 128>>>(leaves_b.as<uint32_t>(), n_leaves, V, owner_b.as<uint32_t>(),
                                                  tets_b.as<tv_tet>(), verts_b.as<uint4>(), stats_b.as<Stats>(), PP,
@@ -1314,6 +1582,13 @@ int build_grid(const float* dens, const float* temp, const float* alb, int nx, i
     return TV_OK;
 #undef CK
 #undef TRY
+}
+}  // namespace
+
+int build_grid(const float* dens, const float* temp, const float* alb, int nx, int ny, int nz,
+               const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out, tv_build_stats* stats) {
+    t_build_device = device;
+    return build_grid_impl(dens, temp, alb, nx, ny, nz, cfg, camera, device, out, stats);
 }
 
 }  // namespace tvb

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -135,7 +136,20 @@ RenderParams make_params(const tv_render_config* r) {
 // Per-device workspace reused across frames (no cudaMalloc in the per-frame
 // path): the per-path buffers of a batch (start records, entry cells,
 // radiance), the accumulators tv_render copies back, the queue counter, and a
-// stream + events. One frame is in flight per device at a time.
+// stream + events.
+//
+// Stream ordering. The render entry points are asynchronous on the caller's
+// stream and every frame on a device shares this workspace, so frames are
+// chained through `idle`: render_frame makes its stream wait for the previous
+// frame's `idle` record before touching the workspace and records `idle` on
+// its own stream after its last kernel. Frames issued on different streams
+// (or tv_render on the workspace's own stream after an asynchronous
+// tv_render_tiles) therefore run one after another on the device, never on
+// the same buffers at once. Host-side buffer growth first waits for `idle`.
+struct TileOrderKey {
+    uint32_t k[4];
+    bool operator<(const TileOrderKey& o) const { return std::lexicographical_compare(k, k + 4, o.k, o.k + 4); }
+};
 struct Workspace {
     std::mutex mu;
     void* paths = nullptr;
@@ -145,20 +159,20 @@ struct Workspace {
     uint32_t* counter = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t idle = nullptr;  // recorded after the last frame's last kernel
     int trace_blocks = 0, sms = 0;
     TraceFn trace = nullptr;
     int trace_threads = kTraceThreads;
     uint32_t regen_min = 8, scatter_min = 8, order = 0;
-    cudaEvent_t tev[4 * 8] = {};  // per-batch kernel boundaries of the last frame
+    std::vector<cudaEvent_t> tev;  // per-batch kernel boundaries of the last frame (4 per batch)
     int n_timed = 0, n_launches = 0;
-    // this rank's tiles, centre first (see tile_order_for)
-    uint32_t* tile_order = nullptr;
-    size_t tile_order_cap = 0;
-    uint32_t tile_key[4] = {0, 0, 0, 0};
+    // per (tiles_x, tiles_y, rank, n_ranks): that rank's tiles in processing
+    // order (see tile_order_for); written once, never overwritten, so frames
+    // still in flight keep reading a valid table
+    std::map<TileOrderKey, uint32_t*> tile_orders;
     int tile_mode = 1;
     double tile_radius = 0.8;  // outer tiles: beyond this fraction of the inscribed circle
 };
-constexpr int kTimedBatches = 8;
 Workspace g_ws[64];
 
 int env_int(const char* name, int dflt) {
@@ -173,20 +187,23 @@ int env_int(const char* name, int dflt) {
 // persistent trace kernel's last chunks are short paths and its tail shrinks.
 // Only the schedule changes: every pixel still accumulates its samples in
 // order. TV_TILE_ORDER: 0 raster always, 1 (default) from 4 ranks up, 2 always.
-int tile_order_for(Workspace& w, uint32_t tiles_x, uint32_t tiles_y, int rank, int n_ranks, const uint32_t*& out) {
+int tile_order_for(Workspace& w, uint32_t tiles_x, uint32_t tiles_y, int rank, int n_ranks, cudaStream_t st,
+                   const uint32_t*& out) {
     out = nullptr;
     // measured on B200 (tools/rank_share.py, C2): the reordering shortens the
     // per-rank tail at 4 and 8 ranks (8.89 vs 9.13 ms per rank at 8) but costs
     // L2 locality on a full frame (+0.3 % at 1 and 2 ranks)
     if (w.tile_mode == 0 || (w.tile_mode == 1 && n_ranks < 4)) return TV_OK;
-    const uint32_t key[4] = {tiles_x, tiles_y, static_cast<uint32_t>(rank), static_cast<uint32_t>(n_ranks)};
-    if (w.tile_order && std::equal(key, key + 4, w.tile_key)) {
-        out = w.tile_order;
+    const TileOrderKey key{{tiles_x, tiles_y, static_cast<uint32_t>(rank), static_cast<uint32_t>(n_ranks)}};
+    auto it = w.tile_orders.find(key);
+    if (it != w.tile_orders.end()) {
+        out = it->second;
         return TV_OK;
     }
     std::vector<uint32_t> tl;
     for (uint32_t t = static_cast<uint32_t>(rank); t < tiles_x * tiles_y; t += static_cast<uint32_t>(n_ranks))
         tl.push_back(t);
+    if (tl.empty()) return TV_OK;
     const double cx = 0.5 * tiles_x, cy = 0.5 * tiles_y;
     const double rr = 0.25 * w.tile_radius * w.tile_radius * std::min(tiles_x, tiles_y) * std::min(tiles_x, tiles_y);
     auto outer = [&](uint32_t t) {
@@ -196,21 +213,27 @@ int tile_order_for(Workspace& w, uint32_t tiles_x, uint32_t tiles_y, int rank, i
     // raster order inside (L2 locality between neighbouring tiles), the outer
     // tiles last
     std::stable_partition(tl.begin(), tl.end(), [&](uint32_t t) { return !outer(t); });
-    if (w.tile_order_cap < tl.size()) {
-        cudaFree(w.tile_order);
-        w.tile_order = nullptr;
-        w.tile_order_cap = 0;
-        TV_CK(cudaMalloc(&w.tile_order, tl.size() * sizeof(uint32_t)), "tile order alloc");
-        w.tile_order_cap = tl.size();
+    if (w.tile_orders.size() >= 64) {  // bounded cache: drop the tables once nothing can read them
+        TV_CK(cudaEventSynchronize(w.idle), "tile order sync");
+        for (auto& kv : w.tile_orders) cudaFree(kv.second);
+        w.tile_orders.clear();
     }
-    TV_CK(cudaMemcpy(w.tile_order, tl.data(), tl.size() * sizeof(uint32_t), cudaMemcpyHostToDevice), "tile order H2D");
-    std::copy(key, key + 4, w.tile_key);
-    out = w.tile_order;
+    uint32_t* d = nullptr;
+    TV_CK(cudaMalloc(&d, tl.size() * sizeof(uint32_t)), "tile order alloc");
+    // stream-ordered upload (a pageable source is staged before the call returns)
+    const cudaError_t e = cudaMemcpyAsync(d, tl.data(), tl.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_status(e, "tile order H2D");
+    }
+    w.tile_orders.emplace(key, d);
+    out = d;
     return TV_OK;
 }
 
-int grow(void*& p, size_t& have, size_t need) {
+int grow(void*& p, size_t& have, size_t need, cudaEvent_t idle) {
     if (have >= need) return TV_OK;
+    if (idle) TV_CK(cudaEventSynchronize(idle), "workspace sync");  // frames in flight may still read p
     cudaFree(p);
     p = nullptr;
     have = 0;
@@ -226,6 +249,8 @@ int workspace(int device, Workspace*& out) {
         TV_CK(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking), "stream create");
         TV_CK(cudaEventCreate(&w.ev0), "event create");
         TV_CK(cudaEventCreate(&w.ev1), "event create");
+        TV_CK(cudaEventCreateWithFlags(&w.idle, cudaEventDisableTiming), "event create");
+        TV_CK(cudaEventRecord(w.idle, w.stream), "event");
         TV_CK(cudaMalloc(&w.counter, 256), "counter alloc");
         // tuning knobs (defaults are the measured best on B200)
         const int maxreg = env_int("TV_TRACE_MAXREG", 72);
@@ -262,28 +287,33 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
     const uint64_t tiles = static_cast<uint64_t>(tiles_x) * tiles_y;
     const uint64_t mine = tiles > static_cast<uint64_t>(rank) ? (tiles - rank + n_ranks - 1) / n_ranks : 0;
     const uint64_t units = mine * 8;
-    const uint32_t* tile_order = nullptr;
-    if (int rc = tile_order_for(w, tiles_x, tiles_y, rank, n_ranks, tile_order)) return rc;
+    w.n_timed = 0;
+    w.n_launches = 0;
     if (units == 0) return TV_OK;
+    // the previous frame on this device (any stream) is done with the workspace
+    TV_CK(cudaStreamWaitEvent(st, w.idle, 0), "wait workspace");
+    const uint32_t* tile_order = nullptr;
+    if (int rc = tile_order_for(w, tiles_x, tiles_y, rank, n_ranks, st, tile_order)) return rc;
     uint64_t ns = std::max<uint64_t>(1, kMaxBatchPaths / (units * 32));
     ns = std::min<uint64_t>(ns, static_cast<uint64_t>(rp.spp));
     if (units * 32 * ns >= (1ull << 31)) return set_error(TV_ERR_ARG, "frame too large for one batch");
     const uint64_t max_paths = units * 32 * ns;
     const size_t need = max_paths * (sizeof(StartRec) + sizeof(uint32_t) + 3 * sizeof(double)) + 256;
-    int rc = grow(w.paths, w.path_bytes, need);
+    int rc = grow(w.paths, w.path_bytes, need, w.idle);
     if (rc) return rc;
     char* base = static_cast<char*>(w.paths);
     StartRec* st_rec = reinterpret_cast<StartRec*>(base);
     double* rad = reinterpret_cast<double*>(base + max_paths * sizeof(StartRec));
     uint32_t* cells = reinterpret_cast<uint32_t*>(base + max_paths * (sizeof(StartRec) + 3 * sizeof(double)));
-    if (!w.tev[0]) {
-        for (auto& e : w.tev) TV_CK(cudaEventCreate(&e), "event create");
+    const uint64_t n_batches = (static_cast<uint64_t>(rp.spp) + ns - 1) / ns;
+    while (w.tev.size() < 4 * n_batches) {
+        cudaEvent_t e;
+        TV_CK(cudaEventCreate(&e), "event create");
+        w.tev.push_back(e);
     }
-    w.n_timed = 0;
-    w.n_launches = 0;
     for (uint64_t s0 = 0; s0 < static_cast<uint64_t>(rp.spp); s0 += ns) {
-        cudaEvent_t* ev = w.n_timed < kTimedBatches ? &w.tev[4 * w.n_timed] : nullptr;
-        if (ev) ++w.n_timed;
+        cudaEvent_t* ev = &w.tev[4 * w.n_timed];
+        ++w.n_timed;
         w.n_launches += 3;
         Batch B;
         B.n_units = static_cast<uint32_t>(units);
@@ -300,21 +330,36 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.order = w.order;
         B.tile_order = tile_order;
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
-        if (ev) TV_CK(cudaEventRecord(ev[0], st), "event");
+        TV_CK(cudaEventRecord(ev[0], st), "event");
         start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);
         TV_CK(cudaGetLastError(), "start_kernel launch");
         TV_CK(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), st), "memset counter");
-        if (ev) TV_CK(cudaEventRecord(ev[1], st), "event");
+        TV_CK(cudaEventRecord(ev[1], st), "event");
         w.trace<<<w.trace_blocks, w.trace_threads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
                                                           w.counter);
         TV_CK(cudaGetLastError(), "trace_kernel launch");
-        if (ev) TV_CK(cudaEventRecord(ev[2], st), "event");
+        TV_CK(cudaEventRecord(ev[2], st), "event");
         const unsigned ab = static_cast<unsigned>(std::min<uint64_t>((units * 32 + 127) / 128, w.sms * 16ull));
         accum_kernel<<<ab, 128, 0, st>>>(B, cv, cells, rad, out);
         TV_CK(cudaGetLastError(), "accum_kernel launch");
-        if (ev) TV_CK(cudaEventRecord(ev[3], st), "event");
+        TV_CK(cudaEventRecord(ev[3], st), "event");
     }
+    TV_CK(cudaEventRecord(w.idle, st), "event");
     return TV_OK;
+}
+
+// 1 when any output buffer lives on another device (mapped with tv_ipc_open)
+int peer_outputs(int device, const void* a, const void* b, const void* c) {
+    for (const void* p : {a, b, c}) {
+        if (!p) continue;
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (at.type == cudaMemoryTypeDevice && at.device != device) return 1;
+    }
+    return 0;
 }
 
 // Device time of the last frame's kernels on this device (sums over batches):
@@ -471,7 +516,7 @@ int tv_render(const tv_grid* h, const tv_camera* camera, const tv_render_config*
     if ((rc = workspace(g.device, w))) return rc;
     std::lock_guard<std::mutex> lk(w->mu);
     const size_t bytes = npx * (3 * sizeof(double) * 2 + sizeof(uint32_t)) + 4 * sizeof(uint64_t) + 256;
-    if ((rc = grow(w->out, w->out_bytes, bytes))) return rc;
+    if ((rc = grow(w->out, w->out_bytes, bytes, w->idle))) return rc;
     Workspace* s = w;
     char* base = static_cast<char*>(w->out);
     double* sum = reinterpret_cast<double*>(base);
@@ -519,7 +564,7 @@ int tv_render_tiles(const tv_grid* h, const tv_camera* camera, const tv_render_c
     Workspace* w;
     if ((rc = workspace(g.device, w))) return rc;
     std::lock_guard<std::mutex> lk(w->mu);
-    RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
+    RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev, peer_outputs(g.device, sum_dev, sum_sq_dev, counts_dev)};
     return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream));
 }
 
@@ -539,7 +584,7 @@ int tv_render_accumulate(const tv_grid* h, const tv_camera* camera, const tv_ren
     Workspace* w;
     if ((rc = workspace(g.device, w))) return rc;
     std::lock_guard<std::mutex> lk(w->mu);
-    RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev};
+    RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev, peer_outputs(g.device, sum_dev, sum_sq_dev, counts_dev)};
     return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream),
                         static_cast<uint32_t>(first_sample));
 }

@@ -1,0 +1,335 @@
+// Diagnostics: the memory-latency ceiling of the trace kernel on a frame
+// (include/tetvol_b200_diag.h).
+//
+// 1. record_kernel runs every path of the frame through the integrator of
+//    trace_path (path_integrator.hpp:42-84), from the same start records
+//    start_kernel gives the render, and writes one 4-bit code per tet step (one
+//    per MarchStep, the reference's cells_visited): the face slot the step
+//    leaves by (0-3), or 4 when the flight collides and the next step re-reads
+//    the same cell. Eight codes per word; each path starts on a word. Two
+//    passes: count, then write at the scanned word offsets.
+// 2. replay_kernel walks the render's paths again as a chain of dependent
+//    64-byte LeafRec loads: each step loads the current leaf's record and takes
+//    the next leaf index from that record's neighbour word named by the code,
+//    exactly the render's dependence (record -> exit face -> neighbour ->
+//    next record) without the geometry. Same path order, block size, per-lane
+//    path regeneration from 64-path warp chunks, and shared-memory footprint
+//    per block (so the same L1 size and resident warps) as the trace kernel.
+//    Its steps/s is the rate of a trace kernel whose exit-face computation
+//    were free.
+#include <algorithm>
+#include <cstdlib>
+#include <cub/cub.cuh>
+#include <vector>
+
+#include "tetvol_b200_diag.h"
+#include "tv_trace.cuh"
+
+namespace tvb {
+
+int validate_render_cfg(const tv_render_config* r);
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// trace_path from a start record (the render's path p), recording or counting
+// the leaf of every step
+__global__ void record_kernel(GridView G, CamView C, RenderParams P, Batch B, const StartRec* __restrict__ st,
+                              const uint32_t* __restrict__ cells, uint32_t* __restrict__ counts,
+                              const uint64_t* __restrict__ offs, uint32_t* __restrict__ codes) {
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= B.n_paths) return;
+    uint32_t cell = cells[p];
+    uint32_t* out = offs ? codes + offs[p] : nullptr;  // word offset of this path
+    uint32_t n = 0, word = 0;
+    if (cell != kNone && cell != kInvalidPixel) {
+        const StartRec sr = st[p];
+        d3 o = mk(C.pos[0], C.pos[1], C.pos[2]);
+        d3 dir = mk(sr.dx, sr.dy, sr.dz);
+        double seg_start = sr.t0, probe = sr.t0 + kNudge;
+        Rng rng;
+        rng.key = sr.key;
+        rng.dim = 3;
+        double target = sr.target;
+        d3 throughput = mk(1, 1, 1);
+        LeafRec rec = load_leaf(G.leaves, cell);
+        for (int bounce = 0;;) {
+            double tau = 0.0;
+            bool collided = false, aborted = false;
+            d3 event = o;
+            for (;;) {
+                if (n + 1 > kMaxSteps) {
+                    aborted = true;
+                    break;
+                }
+                double t;
+                int slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+                if (slot < 0) {
+                    probe += kNudge;
+                    slot = exit_face(rec, ray_at(o, dir, probe), dir, t);
+                    if (slot < 0) {
+                        aborted = true;
+                        break;
+                    }
+                }
+                const double t_exit = dmax(probe + t, seg_start);
+                const double s0 = seg_start, lambda = static_cast<double>(__uint_as_float(rec.w[13]));
+                const uint32_t next = nbr_leaf(sel4(rec.w[0], rec.w[1], rec.w[2], rec.w[3], slot));
+                const double seg_tau = lambda * (t_exit - s0);
+                const bool coll = lambda > 0.0 && tau + seg_tau >= target;
+                if (out) {
+                    word |= static_cast<uint32_t>(coll ? 4 : slot) << (4 * (n & 7));
+                    if ((n & 7) == 7) out[n >> 3] = word, word = 0;
+                }
+                ++n;
+                if (coll) {
+                    event = ray_at(o, dir, s0 + (target - tau) / lambda);
+                    collided = true;
+                    break;
+                }
+                tau += seg_tau;
+                if (next == kNoLeaf) break;
+                rec = load_leaf(G.leaves, next);
+                cell = next;
+                seg_start = t_exit;
+                probe = t_exit + kNudge;
+            }
+            if (aborted || !collided) break;
+            const uint32_t mask = rec.w[12] >> 24;
+            throughput = mul(throughput, (mask & 4u) ? static_cast<double>(__uint_as_float(rec.w[15])) : P.default_albedo);
+            ++bounce;
+            if (bounce >= P.max_bounces) break;
+            if (bounce >= 4) {
+                const double pm = dmax(throughput.x, dmax(throughput.y, throughput.z));
+                if (pm < 1e-3) {
+                    if (rng.next() >= pm) break;
+                    throughput = divs(throughput, pm);
+                }
+            }
+            dir = sample_phase_hg(dir, P.g, rng);
+            o = event;
+            seg_start = 0.0;
+            probe = 0.0;
+            target = -log(1.0 - rng.next());
+        }
+    }
+    if (out && (n & 7)) out[n >> 3] = word;
+    if (!offs) counts[p] = n;
+}
+
+// dependent-gather replay of the recorded paths in render path order
+__global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t* __restrict__ start,
+                              const uint32_t* __restrict__ counts, const uint32_t* __restrict__ codes,
+                              const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t* counter,
+                              uint32_t* sink) {
+    extern __shared__ uint32_t pad[];  // the render's shared-memory footprint (L1 split, blocks per SM)
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t chunk_next = 0, chunk_end = 0;  // warp-uniform
+    bool exhausted = false;                  // warp-uniform
+    uint32_t k = 0, n = 0;                   // this lane's path: step k of n
+    const uint32_t* cw = nullptr;            // its code words
+    uint32_t idx = 0, word = 0, acc = 0;
+    for (;;) {
+        const unsigned idle = __ballot_sync(kFull, k >= n);
+        const bool open = !(exhausted && chunk_next >= chunk_end);
+        if (idle == kFull && !open) break;
+        if (idle && open) {  // idle lanes take the next path ids of the warp's chunk
+            const uint32_t n_idle = __popc(idle), rank = __popc(idle & lt);
+            uint32_t mine = kNone;
+            const uint32_t avail = chunk_end - chunk_next;
+            if (k >= n && rank < avail) mine = chunk_next + rank;
+            const uint32_t used = min(avail, n_idle);
+            chunk_next += used;
+            if (n_idle > avail && !exhausted) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(counter, 64u);
+                base = __shfl_sync(kFull, base, 0);
+                if (base >= n_paths) {
+                    exhausted = true;
+                } else {
+                    chunk_next = base;
+                    chunk_end = min(base + 64u, n_paths);
+                    const uint32_t avail2 = chunk_end - chunk_next;
+                    if (k >= n && mine == kNone && rank - used < avail2) mine = chunk_next + (rank - used);
+                    chunk_next += min(avail2, n_idle - used);
+                }
+            }
+            if (mine != kNone) {
+                k = 0;
+                n = counts[mine];
+                cw = codes + offs[mine];
+                idx = start[mine];
+            }
+        }
+        if (k < n) {
+            if ((k & 7) == 0) word = cw[k >> 3];
+            const LeafRec r = load_leaf(leaves, idx);
+            acc ^= r.w[5] ^ r.w[10] ^ r.w[15];
+            const uint32_t code = (word >> (4 * (k & 7))) & 15u;
+            // the next record's index comes out of this record (as in the render)
+            if (code < 4) idx = nbr_leaf(sel4(r.w[0], r.w[1], r.w[2], r.w[3], static_cast<int>(code)));
+            ++k;
+        }
+    }
+    if (acc == 0x9e3779b9u) sink[0] = acc + pad[0];  // keeps the loads alive
+}
+
+// words of 4-bit codes per path
+__global__ void words_kernel(const uint32_t* in, uint64_t* out, uint64_t n) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = (in[i] + 7u) / 8u;
+}
+
+RenderParams params_of(const tv_render_config* r) {
+    RenderParams p;
+    p.spp = r->spp;
+    p.max_bounces = r->max_bounces;
+    p.seed = r->seed;
+    p.g = r->hg_g;
+    p.default_albedo = r->default_albedo;
+    p.env[0] = r->environment[0], p.env[1] = r->environment[1], p.env[2] = r->environment[2];
+    p.emission_scale = r->emission_scale;
+    return p;
+}
+
+struct Dev {
+    void* p = nullptr;
+    ~Dev() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+}  // namespace tvb
+
+using namespace tvb;
+
+extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera, const tv_render_config* cfg,
+                                      int reps, double out[6]) {
+#define CK(x, what)                                 \
+    do {                                            \
+        if (int rc_ = cuda_status((x), what)) return rc_; \
+    } while (0)
+    if (!h || !out) return set_error(TV_ERR_ARG, "null argument");
+    int rc = validate_render_cfg(cfg);
+    if (rc) return rc;
+    CamView cv;
+    if ((rc = host_camera(camera, cv, nullptr, nullptr))) return rc;
+    const DeviceGrid& g = h->g;
+    if ((rc = use_device(g.device))) return rc;
+    const RenderParams rp = params_of(cfg);
+    // one batch covering the whole frame, laid out exactly as render_frame's
+    const uint32_t tiles_x = (static_cast<uint32_t>(cv.w) + 15) / 16, tiles_y = (static_cast<uint32_t>(cv.h) + 15) / 16;
+    const uint64_t units = static_cast<uint64_t>(tiles_x) * tiles_y * 8;
+    const uint64_t n_paths = units * 32 * static_cast<uint64_t>(rp.spp);
+    if (n_paths >= (1ull << 31) || n_paths > kMaxBatchPaths)
+        return set_error(TV_ERR_ARG, "diag: frame larger than one render batch");
+    Batch B{};
+    B.n_units = static_cast<uint32_t>(units);
+    B.s0 = 0;
+    B.ns = static_cast<uint32_t>(rp.spp);
+    B.tiles_x = tiles_x, B.tiles_y = tiles_y;
+    B.rank = 0, B.n_ranks = 1;
+    B.n_paths = static_cast<uint32_t>(n_paths);
+    B.first = 1;
+    B.order = 1;
+    B.tile_order = nullptr;
+    Dev st, cells, counts, offs, seq, ctr, tmp;
+    CK(cudaMalloc(&st.p, n_paths * sizeof(StartRec)), "diag alloc");
+    CK(cudaMalloc(&cells.p, n_paths * 4), "diag alloc");
+    CK(cudaMalloc(&counts.p, n_paths * 4), "diag alloc");
+    CK(cudaMalloc(&offs.p, (n_paths + 1) * 8), "diag alloc");
+    CK(cudaMalloc(&ctr.p, 256), "diag alloc");
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.device);
+    start_kernel<<<static_cast<unsigned>(std::min<uint64_t>((n_paths + 255) / 256, sms * 16ull)), 256>>>(
+        g.view, cv, rp, B, static_cast<StartRec*>(st.p), static_cast<uint32_t*>(cells.p));
+    CK(cudaGetLastError(), "diag start");
+    const unsigned rb = static_cast<unsigned>((n_paths + 127) / 128);
+    record_kernel<<<rb, 128>>>(g.view, cv, rp, B, static_cast<const StartRec*>(st.p),
+                               static_cast<const uint32_t*>(cells.p), static_cast<uint32_t*>(counts.p), nullptr,
+                               nullptr);
+    CK(cudaGetLastError(), "diag count");
+    // offsets = exclusive scan of the counts (64-bit)
+    CK(cudaMemset(offs.p, 0, 8), "diag");
+    words_kernel<<<static_cast<unsigned>((n_paths + 255) / 256), 256>>>(static_cast<const uint32_t*>(counts.p),
+                                                                        static_cast<uint64_t*>(offs.p) + 1, n_paths);
+    {
+        uint64_t* o1 = static_cast<uint64_t*>(offs.p) + 1;
+        size_t tb = 0;
+        CK(cub::DeviceScan::InclusiveSum(nullptr, tb, o1, o1, static_cast<int64_t>(n_paths)), "diag scan");
+        CK(cudaMalloc(&tmp.p, tb), "diag alloc");
+        CK(cub::DeviceScan::InclusiveSum(tmp.p, tb, o1, o1, static_cast<int64_t>(n_paths)), "diag scan");
+    }
+    // total steps (counts summed on the device)
+    uint64_t total = 0;
+    {
+        Dev sum_d, tmp2;
+        CK(cudaMalloc(&sum_d.p, 8), "diag alloc");
+        auto in = static_cast<const uint32_t*>(counts.p);
+        size_t tb = 0;
+        CK(cub::DeviceReduce::Sum(nullptr, tb, in, static_cast<uint64_t*>(sum_d.p), static_cast<int64_t>(n_paths)),
+           "diag sum");
+        CK(cudaMalloc(&tmp2.p, tb), "diag alloc");
+        CK(cub::DeviceReduce::Sum(tmp2.p, tb, in, static_cast<uint64_t*>(sum_d.p), static_cast<int64_t>(n_paths)),
+           "diag sum");
+        CK(cudaMemcpy(&total, sum_d.p, 8, cudaMemcpyDeviceToHost), "diag");
+    }
+    uint64_t words = 0;
+    CK(cudaMemcpy(&words, static_cast<uint64_t*>(offs.p) + n_paths, 8, cudaMemcpyDeviceToHost), "diag");
+    CK(cudaMalloc(&seq.p, std::max<uint64_t>(words, 1) * 4), "diag alloc (4 bits per tet step)");
+    record_kernel<<<rb, 128>>>(g.view, cv, rp, B, static_cast<const StartRec*>(st.p),
+                               static_cast<const uint32_t*>(cells.p), nullptr, static_cast<const uint64_t*>(offs.p),
+                               static_cast<uint32_t*>(seq.p));
+    CK(cudaGetLastError(), "diag record");
+    CK(cudaDeviceSynchronize(), "diag record");
+    // replay with the render's launch shape: 128 threads, its shared memory
+    // per block and carveout (hence the same L1 and blocks per SM), then with
+    // every warp slot of the SM filled
+    const size_t trace_smem = sizeof(FaceTables<kTraceThreads>) + sizeof(double) * 6 * kTraceThreads +
+                              sizeof(unsigned long long) * kTraceThreads + 3 * sizeof(uint32_t) * kTraceThreads;
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(replay_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(trace_smem));
+    const char* cv_env = std::getenv("TV_CARVEOUT");
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(replay_kernel), cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cv_env && *cv_env ? std::atoi(cv_env) : 72);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best[2] = {1e30, 1e30};
+    int warps[2] = {0, 0};
+    for (int mode = 0; mode < 2; ++mode) {
+        const size_t smem = mode == 0 ? trace_smem : 0;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(replay_kernel), 128, smem);
+        warps[mode] = per_sm * 4;
+        const unsigned blocks = static_cast<unsigned>(sms * std::max(per_sm, 1));
+        for (int r = 0; r < std::max(reps, 1); ++r) {
+            CK(cudaMemset(ctr.p, 0, 256), "diag");
+            cudaEventRecord(e0);
+            replay_kernel<<<blocks, 128, smem>>>(g.leaves, static_cast<const uint32_t*>(cells.p),
+                                                 static_cast<const uint32_t*>(counts.p),
+                                                 static_cast<const uint32_t*>(seq.p),
+                                                 static_cast<const uint64_t*>(offs.p), B.n_paths,
+                                                 static_cast<uint32_t*>(ctr.p), static_cast<uint32_t*>(ctr.p) + 32);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1), "diag replay");
+            CK(cudaGetLastError(), "diag replay");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best[mode] = std::min(best[mode], static_cast<double>(ms));
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    out[0] = total / (best[0] * 1e-3);
+    out[1] = total / (best[1] * 1e-3);
+    out[2] = static_cast<double>(total);
+    out[3] = best[0];
+    out[4] = 0.5;
+    out[5] = warps[0];
+    return TV_OK;
+#undef CK
+}

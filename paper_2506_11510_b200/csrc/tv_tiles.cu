@@ -4,6 +4,7 @@
 // block of ceil(tiles / n_ranks) * 256 pixels (equal size on every rank, so one
 // NCCL all-gather moves the frame); unpack scatters a gathered block back.
 #include <algorithm>
+#include <cstring>
 
 #include "tv_trace.cuh"
 
@@ -64,6 +65,37 @@ int tv_tile_pack(const void* frame_dev, void* packed_dev, int32_t width, int32_t
 int tv_tile_unpack(const void* packed_dev, void* frame_dev, int32_t width, int32_t height, int32_t rank,
                    int32_t n_ranks, int32_t elem_words, void* stream) {
     return tvb::run(frame_dev, const_cast<void*>(packed_dev), width, height, rank, n_ranks, elem_words, stream, 1);
+}
+
+int tv_ipc_export(const void* dev_ptr, uint8_t handle[64]) {
+    if (!dev_ptr || !handle) return tvb::set_error(TV_ERR_ARG, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, dev_ptr);
+    if (e != cudaSuccess || a.type != cudaMemoryTypeDevice)
+        return tvb::set_error(TV_ERR_ARG, "ipc export: not a device pointer");
+    if ((e = cudaSetDevice(a.device)) != cudaSuccess) return tvb::cuda_status(e, "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    if (e != cudaSuccess) return tvb::cuda_status(e, "cudaIpcGetMemHandle");
+    std::memcpy(handle, &h, 64);
+    return TV_OK;
+}
+
+int tv_ipc_open(const uint8_t handle[64], int device, void** dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return tvb::set_error(TV_ERR_ARG, "null argument");
+    *dev_ptr_out = nullptr;
+    int rc = tvb::use_device(device);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    return tvb::cuda_status(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess),
+                            "cudaIpcOpenMemHandle");
+}
+
+int tv_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return TV_OK;
+    return tvb::cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

@@ -142,6 +142,9 @@ __global__ void accum_kernel(Batch B, CamView C, const uint32_t* __restrict__ ce
         if (O.sum_sq) O.sum_sq[3 * pix] = qr, O.sum_sq[3 * pix + 1] = qg, O.sum_sq[3 * pix + 2] = qb;
         if (O.counts) O.counts[pix] = n;
     }
+    // peer outputs (tv_ipc_open): publish this thread's stores before the
+    // kernel ends, so a stream-ordered barrier after it covers them
+    if (O.remote) __threadfence_system();
     if (O.stats) {
         for (int o = 16; o; o >>= 1) traced += __shfl_down_sync(kFull, traced, o);
         if ((threadIdx.x & 31) == 0 && traced) atomicAdd(reinterpret_cast<unsigned long long*>(O.stats + 1), traced);

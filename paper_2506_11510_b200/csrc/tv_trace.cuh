@@ -42,6 +42,7 @@ struct RenderOut {
     double* sum_sq;
     uint32_t* counts;
     uint64_t* stats;  // [cells_visited, paths_traced, degenerate_paths]
+    int remote;       // outputs live on a peer GPU: fence the stores system-wide
 };
 
 __global__ void start_kernel(GridView G, CamView C, RenderParams P, Batch B, StartRec* st, uint32_t* cells);

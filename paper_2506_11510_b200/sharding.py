@@ -7,6 +7,11 @@ render each rank packs its tiles into an equal-size block (ceil(tiles /
 n_ranks) * 256 pixel slots), one all-gather moves the blocks, and every block
 is scattered back. This module is the host-side mirror of the device pack /
 unpack kernels (csrc/tv_tiles.cu), used by bench.py and by the CPU gloo tests.
+
+PeerFrame is the fused alternative: rank 0's full-frame accumulators are mapped
+into every rank (CUDA IPC), each rank's accumulate kernel stores its pixels
+straight into them over NVLink, and a stream-ordered one-word all-reduce is the
+only collective (a completion barrier, no pixel data).
 """
 from __future__ import annotations
 
@@ -60,3 +65,39 @@ def owner_map(width: int, height: int, n_ranks: int) -> np.ndarray:
     tx, _ = n_tiles(width, height)
     y, x = np.mgrid[0:height, 0:width]
     return ((y // TILE) * tx + x // TILE) % n_ranks
+
+
+class PeerFrame:
+    """Rank 0's frame accumulators (sum, sum_sq: 3 doubles per pixel; counts: u32
+    per pixel), mapped on every rank of `group` through tv_ipc_export /
+    tv_ipc_open. `ptrs` are this rank's device pointers to them."""
+
+    def __init__(self, width: int, height: int, rank: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        import paper_2506_11510_b200 as tv
+
+        npx = width * height
+        self.rank, self.device, self.mapped = rank, device, []
+        self.local = None
+        handles = [None, None, None]
+        if rank == 0:
+            self.local = (torch.zeros(npx * 3, dtype=torch.float64, device=f"cuda:{device}"),
+                          torch.zeros(npx * 3, dtype=torch.float64, device=f"cuda:{device}"),
+                          torch.zeros(npx, dtype=torch.int32, device=f"cuda:{device}"))
+            handles = [tv.ipc_export(t.data_ptr()) for t in self.local]
+        box = [handles]
+        dist.broadcast_object_list(box, src=0, group=group)
+        if rank == 0:
+            self.ptrs = tuple(t.data_ptr() for t in self.local)
+        else:
+            self.mapped = [tv.ipc_open(h, device) for h in box[0]]
+            self.ptrs = tuple(self.mapped)
+
+    def close(self):
+        import paper_2506_11510_b200 as tv
+
+        for p in self.mapped:
+            tv.ipc_close(p)
+        self.mapped = []

@@ -127,3 +127,44 @@ def test_build_config_errors(tv):
         tv.build_adaptive_grid(vol, tv.BuildConfig(max_level=49))
     with pytest.raises(tv.ConfigError, match="useCamera"):
         tv.build_adaptive_grid(vol, tv.BuildConfig(use_camera=True))
+
+
+def test_build_leaves_the_default_mempool_alone(tv):
+    """Build scratch lives in a private pool that is trimmed after the build
+    (ADVICE r01): the device's default pool keeps its release threshold, and
+    two builds of the same field give identical grids (determinism)."""
+    from cuda.bindings import runtime as rt
+
+    err, pool = rt.cudaDeviceGetDefaultMemPool(0)
+    assert err == rt.cudaError_t.cudaSuccess
+    attr = rt.cudaMemPoolAttr.cudaMemPoolAttrReleaseThreshold
+    err, before = rt.cudaMemPoolGetAttribute(pool, attr)
+    vol = O.gen_volume("cloud", 48)
+    bc = tv.BuildConfig(0.3, 12, False, 1.0, 8.0)
+    g1, s1 = tv.build_adaptive_grid(vol, bc)
+    g2, s2 = tv.build_adaptive_grid(vol, bc)
+    err, after = rt.cudaMemPoolGetAttribute(pool, attr)
+    assert int(after) == int(before)
+    v1, t1, r1 = g1.download()
+    v2, t2, r2 = g2.download()
+    assert s1.leaf_count == s2.leaf_count
+    assert np.array_equal(v1, v2) and np.array_equal(t1.view(np.uint8), t2.view(np.uint8))
+
+
+def test_build_from_misaligned_device_volume(tv):
+    """tv_build_dev reads the volume as float4; a channel pointer that is not
+    16-byte aligned is copied first and builds the same grid."""
+    import torch
+
+    vol = O.gen_volume("cloud", 40)
+    flat = torch.from_numpy(np.ascontiguousarray(vol).reshape(-1)).cuda()
+    shifted = torch.zeros(flat.numel() + 1, dtype=torch.float32, device="cuda")
+    shifted[1:] = flat
+    bc = tv.BuildConfig(0.3, 12, False, 1.0, 8.0)
+    g1, s1 = tv.build_adaptive_grid_dev(flat.data_ptr(), (40, 40, 40), bc)
+    g2, s2 = tv.build_adaptive_grid_dev(shifted[1:].data_ptr(), (40, 40, 40), bc)
+    assert shifted[1:].data_ptr() % 16 != 0
+    v1, t1, _ = g1.download()
+    v2, t2, _ = g2.download()
+    assert s1.leaf_count == s2.leaf_count
+    assert np.array_equal(v1, v2) and np.array_equal(t1.view(np.uint8), t2.view(np.uint8))
