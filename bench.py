@@ -200,6 +200,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather", action="store_true", help="use the multi-GPU tile gather path even on one rank")
+    ap.add_argument("--gather-mode", default="nccl", choices=["nccl", "p2p"],
+                    help="multi-GPU frame assembly: NCCL all-gather of packed tiles, or direct peer writes of every "
+                         "rank's pixels into rank 0's accumulators (CUDA IPC) with a one-word all-reduce barrier")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -240,15 +243,25 @@ def main():
     gathered = torch.zeros(words * world, dtype=torch.float64, device="cuda")
     k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    p2p = multi and args.gather_mode == "p2p"
+    out_ptrs = (sum_.data_ptr(), sum_sq.data_ptr(), counts.data_ptr())
+    if p2p:  # every rank's accumulate kernel writes into rank 0's frame over NVLink
+        peer = sharding.PeerFrame(W_IMG, H_IMG, rank, dev)
+        out_ptrs = peer.ptrs
+        if rank == 0:
+            sum_ = peer.local[0]
+        fence = torch.zeros(1, dtype=torch.float32, device="cuda")
 
     def step(i, timed=False):
         if timed:
             k_start[i].record(stream)
-        tv.render_tiles(grid, cam, rc, rank, world, sum_.data_ptr(), sum_sq.data_ptr(), counts.data_ptr(),
-                        stats.data_ptr(), sh)
+        tv.render_tiles(grid, cam, rc, rank, world, out_ptrs[0], out_ptrs[1], out_ptrs[2], stats.data_ptr(), sh)
         if timed:
             k_end[i].record(stream)
-        if multi:
+        if p2p:
+            with torch.cuda.stream(stream):  # completion barrier: every rank's pixels have landed
+                dist.all_reduce(fence)
+        elif multi:
             tv.tile_pack(sum_.data_ptr(), packed.data_ptr(), W_IMG, H_IMG, rank, world, 3, sh)
             with torch.cuda.stream(stream):
                 dist.all_gather_into_tensor(gathered, packed)
@@ -331,7 +344,9 @@ def main():
         e2e_s = float(e2[0])
         e2e = {"value": samples / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": 96 + 88,
                "d2h_bytes_per_step": npx * 24, "ms_per_step": e2e_s * 1e3,
-               "path": "tv_render_tiles + NCCL all-gather of packed tiles + D2H of the frame sums on rank 0"}
+               "path": ("tv_render_tiles writing rank 0's frame over NVLink (P2P) + one-word all-reduce barrier"
+                        if p2p else "tv_render_tiles + NCCL all-gather of packed tiles") +
+                       " + D2H of the frame sums on rank 0"}
 
     pk = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
@@ -400,12 +415,15 @@ def main():
                        "build_s_device": bst.seconds},
             "tet_steps_per_s": cells_frame / (ms * 1e-3), "cells_per_path": cells_frame / samples,
             "ms_per_frame": ms, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
-            "gpu_launches": (timing["launches"] + (1 + world if multi else 0)) * args.steps,
+            "gpu_launches": (timing["launches"] + (0 if p2p else (1 + world if multi else 0))) * args.steps,
+            "gather_mode": args.gather_mode if multi else None,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if multi:
         dist.barrier()
+        if p2p:
+            peer.close()
         dist.destroy_process_group()
 
 

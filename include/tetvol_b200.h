@@ -259,10 +259,12 @@ int tv_tile_unpack(const void* packed_dev, void* frame_dev, int32_t width, int32
  * all-gather or unpack). tv_render_tiles detects peer outputs and ends the
  * accumulate kernel with a system-scope fence, so a stream-ordered barrier
  * after it (e.g. a one-word NCCL all-reduce) publishes the pixels. The handle
- * is 64 opaque bytes (cudaIpcMemHandle_t). */
-int tv_ipc_export(const void* dev_ptr, uint8_t handle[64]);
-int tv_ipc_open(const uint8_t handle[64], int device, void** dev_ptr_out);
-int tv_ipc_close(void* dev_ptr);
+ * is 64 opaque bytes (cudaIpcMemHandle_t) naming the whole allocation that
+ * holds dev_ptr, and offset is dev_ptr's byte offset inside it (allocators
+ * such as PyTorch's hand out sub-ranges of larger allocations). */
+int tv_ipc_export(const void* dev_ptr, uint8_t handle[64], uint64_t* offset);
+int tv_ipc_open(const uint8_t handle[64], uint64_t offset, int device, void** dev_ptr_out);
+int tv_ipc_close(void* dev_ptr, uint64_t offset); /* dev_ptr, offset as from tv_ipc_open */
 
 /* -- volumes in HBM (DenseVolume, volume.hpp:19-58; .dvol, volume.cpp:84-138) -- */
 /* create: a zero "density" channel (volume.hpp:25); dims in [1, 4096].       */

@@ -177,9 +177,9 @@ _sig("tv_render_regular", C.c_int, _F, C.c_int32, C.c_int32, C.c_int32, C.c_doub
 _sig("tv_render_regular_dev", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
      C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
 
-_sig("tv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8))
-_sig("tv_ipc_open", C.c_int, C.POINTER(C.c_uint8), C.c_int, C.POINTER(_P))
-_sig("tv_ipc_close", C.c_int, _P)
+_sig("tv_ipc_export", C.c_int, _P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64))
+_sig("tv_ipc_open", C.c_int, C.POINTER(C.c_uint8), C.c_uint64, C.c_int, C.POINTER(_P))
+_sig("tv_ipc_close", C.c_int, _P, C.c_uint64)
 _sig("tv_diag_gather_ceiling", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.c_int,
      C.POINTER(C.c_double))
 
@@ -447,22 +447,23 @@ def diag_gather_ceiling(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig,
 
 
 def ipc_export(dev_ptr: int) -> bytes:
-    """64-byte handle of a device allocation, for tv_ipc_open in another process."""
+    """Handle (64 bytes) + byte offset (8) of a device pointer, for ipc_open in another process."""
     h = (C.c_uint8 * 64)()
-    _check(_lib.tv_ipc_export(C.c_void_p(dev_ptr), h))
-    return bytes(h)
+    off = C.c_uint64()
+    _check(_lib.tv_ipc_export(C.c_void_p(dev_ptr), h, C.byref(off)))
+    return bytes(h) + int(off.value).to_bytes(8, "little")
 
 
 def ipc_open(handle: bytes, device: int = 0) -> int:
-    """Maps a peer process's allocation (tv_ipc_export) on `device`; returns the device pointer."""
-    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    """Maps a peer process's pointer (ipc_export) on `device`; returns the device pointer."""
+    h = (C.c_uint8 * 64).from_buffer_copy(handle[:64])
     out = C.c_void_p()
-    _check(_lib.tv_ipc_open(h, int(device), C.byref(out)))
+    _check(_lib.tv_ipc_open(h, int.from_bytes(handle[64:72], "little"), int(device), C.byref(out)))
     return int(out.value)
 
 
-def ipc_close(dev_ptr: int) -> None:
-    _check(_lib.tv_ipc_close(C.c_void_p(dev_ptr)))
+def ipc_close(dev_ptr: int, handle: bytes) -> None:
+    _check(_lib.tv_ipc_close(C.c_void_p(dev_ptr), int.from_bytes(handle[64:72], "little")))
 
 
 def tile_pack_words(width: int, height: int, rank: int, n_ranks: int, elem_words: int) -> int:

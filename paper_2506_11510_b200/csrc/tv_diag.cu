@@ -118,28 +118,36 @@ __global__ void record_kernel(GridView G, CamView C, RenderParams P, Batch B, co
     if (!offs) counts[p] = n;
 }
 
-// dependent-gather replay of the recorded paths in render path order
+// dependent-gather replay of the recorded paths in render path order, with
+// the trace kernel's warp schedule: idle lanes regenerate in batches
+// (regen_min), lanes whose flight collided wait for a scatter batch
+// (scatter_min), and the stepping lanes step until one changes state
 __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t* __restrict__ start,
                               const uint32_t* __restrict__ counts, const uint32_t* __restrict__ codes,
-                              const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t* counter,
-                              uint32_t* sink) {
+                              const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t regen_min,
+                              uint32_t scatter_min, uint32_t* counter, uint32_t* sink) {
     extern __shared__ uint32_t pad[];  // the render's shared-memory footprint (L1 split, blocks per SM)
+    enum : int { IDLE = 0, STEP = 1, WAIT = 2 };
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     uint32_t chunk_next = 0, chunk_end = 0;  // warp-uniform
     bool exhausted = false;                  // warp-uniform
-    uint32_t k = 0, n = 0;                   // this lane's path: step k of n
-    const uint32_t* cw = nullptr;            // its code words
+    int state = IDLE;
+    uint32_t k = 0, n = 0;          // this lane's path: step k of n
+    const uint32_t* cw = nullptr;   // its code words
     uint32_t idx = 0, word = 0, acc = 0;
     for (;;) {
-        const unsigned idle = __ballot_sync(kFull, k >= n);
+        const unsigned idle = __ballot_sync(kFull, state == IDLE);
+        const unsigned stepping = __ballot_sync(kFull, state == STEP);
+        const unsigned waiting = __ballot_sync(kFull, state == WAIT);
         const bool open = !(exhausted && chunk_next >= chunk_end);
-        if (idle == kFull && !open) break;
-        if (idle && open) {  // idle lanes take the next path ids of the warp's chunk
-            const uint32_t n_idle = __popc(idle), rank = __popc(idle & lt);
+        if (!stepping && !waiting && !open) break;
+        const uint32_t n_idle = __popc(idle);
+        if (n_idle && open && (n_idle >= regen_min || !stepping)) {
+            const uint32_t rank = __popc(idle & lt);
             uint32_t mine = kNone;
             const uint32_t avail = chunk_end - chunk_next;
-            if (k >= n && rank < avail) mine = chunk_next + rank;
+            if (state == IDLE && rank < avail) mine = chunk_next + rank;
             const uint32_t used = min(avail, n_idle);
             chunk_next += used;
             if (n_idle > avail && !exhausted) {
@@ -152,7 +160,7 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
                     chunk_next = base;
                     chunk_end = min(base + 64u, n_paths);
                     const uint32_t avail2 = chunk_end - chunk_next;
-                    if (k >= n && mine == kNone && rank - used < avail2) mine = chunk_next + (rank - used);
+                    if (state == IDLE && mine == kNone && rank - used < avail2) mine = chunk_next + (rank - used);
                     chunk_next += min(avail2, n_idle - used);
                 }
             }
@@ -161,16 +169,26 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
                 n = counts[mine];
                 cw = codes + offs[mine];
                 idx = start[mine];
+                state = n ? STEP : IDLE;
             }
         }
-        if (k < n) {
-            if ((k & 7) == 0) word = cw[k >> 3];
-            const LeafRec r = load_leaf(leaves, idx);
-            acc ^= r.w[5] ^ r.w[10] ^ r.w[15];
-            const uint32_t code = (word >> (4 * (k & 7))) & 15u;
-            // the next record's index comes out of this record (as in the render)
-            if (code < 4) idx = nbr_leaf(sel4(r.w[0], r.w[1], r.w[2], r.w[3], static_cast<int>(code)));
-            ++k;
+        if (waiting && (static_cast<uint32_t>(__popc(waiting)) >= scatter_min || !stepping))
+            if (state == WAIT) state = k < n ? STEP : IDLE;
+        const unsigned run = __ballot_sync(kFull, state == STEP);
+        if (!run) continue;
+        for (;;) {
+            if (state == STEP) {
+                if ((k & 7) == 0) word = cw[k >> 3];
+                const LeafRec r = load_leaf(leaves, idx);
+                acc ^= r.w[5] ^ r.w[10] ^ r.w[15];
+                const uint32_t code = (word >> (4 * (k & 7))) & 15u;
+                ++k;
+                // the next record's index comes out of this record (as in the render)
+                if (code < 4) idx = nbr_leaf(sel4(r.w[0], r.w[1], r.w[2], r.w[3], static_cast<int>(code)));
+                if (k >= n) state = IDLE;
+                else if (code == 4) state = WAIT;  // collision: the scatter batch, then the same cell
+            }
+            if (__ballot_sync(kFull, state == STEP) != run) break;
         }
     }
     if (acc == 0x9e3779b9u) sink[0] = acc + pad[0];  // keeps the loads alive
@@ -288,13 +306,20 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
     // replay with the render's launch shape: 128 threads, its shared memory
     // per block and carveout (hence the same L1 and blocks per SM), then with
     // every warp slot of the SM filled
-    const size_t trace_smem = sizeof(FaceTables<kTraceThreads>) + sizeof(double) * 6 * kTraceThreads +
-                              sizeof(unsigned long long) * kTraceThreads + 3 * sizeof(uint32_t) * kTraceThreads;
+    size_t trace_smem = sizeof(FaceTables<kTraceThreads>) + sizeof(double) * 6 * kTraceThreads +
+                        sizeof(unsigned long long) * kTraceThreads + 3 * sizeof(uint32_t) * kTraceThreads;
+    // what-if knobs (dev): shared-memory footprint per block and carveout of the first replay
+    if (const char* v = std::getenv("TV_DIAG_SMEM")) trace_smem = static_cast<size_t>(std::atol(v));
     cudaFuncSetAttribute(reinterpret_cast<const void*>(replay_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(trace_smem));
-    const char* cv_env = std::getenv("TV_CARVEOUT");
+    const char* cv_env = std::getenv("TV_DIAG_CARVEOUT") ? std::getenv("TV_DIAG_CARVEOUT") : std::getenv("TV_CARVEOUT");
     cudaFuncSetAttribute(reinterpret_cast<const void*>(replay_kernel), cudaFuncAttributePreferredSharedMemoryCarveout,
                          cv_env && *cv_env ? std::atoi(cv_env) : 72);
+    auto env_u = [](const char* name, uint32_t d) {
+        const char* v = std::getenv(name);
+        return v && *v ? static_cast<uint32_t>(std::atoi(v)) : d;
+    };
+    const uint32_t regen_min = env_u("TV_REGEN_MIN", 5), scatter_min = env_u("TV_SCATTER_MIN", 2);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -312,8 +337,9 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
             replay_kernel<<<blocks, 128, smem>>>(g.leaves, static_cast<const uint32_t*>(cells.p),
                                                  static_cast<const uint32_t*>(counts.p),
                                                  static_cast<const uint32_t*>(seq.p),
-                                                 static_cast<const uint64_t*>(offs.p), B.n_paths,
-                                                 static_cast<uint32_t*>(ctr.p), static_cast<uint32_t*>(ctr.p) + 32);
+                                                 static_cast<const uint64_t*>(offs.p), B.n_paths, regen_min,
+                                                 scatter_min, static_cast<uint32_t*>(ctr.p),
+                                                 static_cast<uint32_t*>(ctr.p) + 32);
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1), "diag replay");
             CK(cudaGetLastError(), "diag replay");

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cuda.h>
+
 #include "tv_trace.cuh"
 
 namespace tvb {
@@ -67,35 +69,54 @@ int tv_tile_unpack(const void* packed_dev, void* frame_dev, int32_t width, int32
     return tvb::run(frame_dev, const_cast<void*>(packed_dev), width, height, rank, n_ranks, elem_words, stream, 1);
 }
 
-int tv_ipc_export(const void* dev_ptr, uint8_t handle[64]) {
-    if (!dev_ptr || !handle) return tvb::set_error(TV_ERR_ARG, "null argument");
+int tv_ipc_export(const void* dev_ptr, uint8_t handle[64], uint64_t* offset) {
+    if (!dev_ptr || !handle || !offset) return tvb::set_error(TV_ERR_ARG, "null argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
     cudaPointerAttributes a;
     cudaError_t e = cudaPointerGetAttributes(&a, dev_ptr);
     if (e != cudaSuccess || a.type != cudaMemoryTypeDevice)
         return tvb::set_error(TV_ERR_ARG, "ipc export: not a device pointer");
     if ((e = cudaSetDevice(a.device)) != cudaSuccess) return tvb::cuda_status(e, "cudaSetDevice");
+    // the handle names the allocation containing dev_ptr: find its base
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<GetRange>(fn);
+    }();
+    if (!get_range) return tvb::set_error(TV_ERR_CUDA, "ipc export: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return tvb::set_error(TV_ERR_CUDA, "ipc export: cuMemGetAddressRange failed");
     cudaIpcMemHandle_t h;
-    e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+    e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
     if (e != cudaSuccess) return tvb::cuda_status(e, "cudaIpcGetMemHandle");
     std::memcpy(handle, &h, 64);
+    *offset = reinterpret_cast<CUdeviceptr>(dev_ptr) - base;
     return TV_OK;
 }
 
-int tv_ipc_open(const uint8_t handle[64], int device, void** dev_ptr_out) {
+int tv_ipc_open(const uint8_t handle[64], uint64_t offset, int device, void** dev_ptr_out) {
     if (!handle || !dev_ptr_out) return tvb::set_error(TV_ERR_ARG, "null argument");
     *dev_ptr_out = nullptr;
     int rc = tvb::use_device(device);
     if (rc) return rc;
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle, 64);
-    return tvb::cuda_status(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess),
-                            "cudaIpcOpenMemHandle");
+    void* base = nullptr;
+    rc = tvb::cuda_status(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    if (rc) return rc;
+    *dev_ptr_out = static_cast<char*>(base) + offset;
+    return TV_OK;
 }
 
-int tv_ipc_close(void* dev_ptr) {
+int tv_ipc_close(void* dev_ptr, uint64_t offset) {
     if (!dev_ptr) return TV_OK;
-    return tvb::cuda_status(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+    return tvb::cuda_status(cudaIpcCloseMemHandle(static_cast<char*>(dev_ptr) - offset), "cudaIpcCloseMemHandle");
 }
 
 }  // extern "C"

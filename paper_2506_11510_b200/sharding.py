@@ -92,12 +92,12 @@ class PeerFrame:
         if rank == 0:
             self.ptrs = tuple(t.data_ptr() for t in self.local)
         else:
-            self.mapped = [tv.ipc_open(h, device) for h in box[0]]
-            self.ptrs = tuple(self.mapped)
+            self.mapped = [(tv.ipc_open(h, device), h) for h in box[0]]
+            self.ptrs = tuple(p for p, _ in self.mapped)
 
     def close(self):
         import paper_2506_11510_b200 as tv
 
-        for p in self.mapped:
-            tv.ipc_close(p)
+        for p, h in self.mapped:
+            tv.ipc_close(p, h)
         self.mapped = []
