@@ -9,8 +9,12 @@ is how this benchmark satisfies the L2 rule (no flush between steps).
 
 With --gpus N (torchrun, one rank per GPU) every rank holds a replica of the
 grid and renders the interleaved 16x16 tiles t with t % N == rank of the SAME
-frame (strong scaling); the tiles are packed and all-gathered over NCCL and
-unpacked into the full frame on every rank, inside the timed step.
+frame (strong scaling). Frame assembly is inside the timed step: by default
+(--gather-mode p2p) every rank's accumulate kernel stores its pixels straight
+into rank 0's frame buffers over NVLink (CUDA IPC mappings) and a one-word
+NCCL all-reduce on the render stream is the completion barrier; with
+--gather-mode nccl (also the automatic fallback when peer mappings fail) the
+tiles are packed, all-gathered over NCCL and unpacked on every rank.
 
 --impl reference times the reference's own CPU renderer (oracle/_ref, compiled
 from /root/reference) on this box's host cores on a bounded sample of the same
@@ -200,7 +204,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gather", action="store_true", help="use the multi-GPU tile gather path even on one rank")
-    ap.add_argument("--gather-mode", default="nccl", choices=["nccl", "p2p"],
+    ap.add_argument("--gather-mode", default="p2p", choices=["nccl", "p2p"],
                     help="multi-GPU frame assembly: NCCL all-gather of packed tiles, or direct peer writes of every "
                          "rank's pixels into rank 0's accumulators (CUDA IPC) with a one-word all-reduce barrier")
     args = ap.parse_args()
@@ -245,12 +249,24 @@ def main():
     k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     p2p = multi and args.gather_mode == "p2p"
     out_ptrs = (sum_.data_ptr(), sum_sq.data_ptr(), counts.data_ptr())
+    gather_note = None
     if p2p:  # every rank's accumulate kernel writes into rank 0's frame over NVLink
-        peer = sharding.PeerFrame(W_IMG, H_IMG, rank, dev)
-        out_ptrs = peer.ptrs
-        if rank == 0:
-            sum_ = peer.local[0]
-        fence = torch.zeros(1, dtype=torch.float32, device="cuda")
+        try:
+            peer = sharding.PeerFrame(W_IMG, H_IMG, rank, dev)
+            ok = torch.ones(1, device="cuda")
+        except Exception as e:  # e.g. no peer access between these GPUs: the NCCL gather instead
+            peer, ok, gather_note = None, torch.zeros(1, device="cuda"), f"p2p unavailable ({e!r}); NCCL all-gather"
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if float(ok[0]) == 0.0:
+            if peer is not None:
+                peer.close()
+            p2p, args.gather_mode = False, "nccl"
+            gather_note = gather_note or "p2p unavailable on some rank; NCCL all-gather"
+        else:
+            out_ptrs = peer.ptrs
+            if rank == 0:
+                sum_ = peer.local[0]
+            fence = torch.zeros(1, dtype=torch.float32, device="cuda")
 
     def step(i, timed=False):
         if timed:
@@ -416,7 +432,7 @@ def main():
             "tet_steps_per_s": cells_frame / (ms * 1e-3), "cells_per_path": cells_frame / samples,
             "ms_per_frame": ms, "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "gpu_launches": (timing["launches"] + (0 if p2p else (1 + world if multi else 0))) * args.steps,
-            "gather_mode": args.gather_mode if multi else None,
+            "gather_mode": args.gather_mode if multi else None, "gather_note": gather_note,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -157,6 +157,7 @@ struct Workspace {
     void* out = nullptr;
     size_t out_bytes = 0;
     uint32_t* counter = nullptr;
+    void* cold = nullptr;  // trace kernel cold path state, kColdBytes per resident thread
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t idle = nullptr;  // recorded after the last frame's last kernel
@@ -267,6 +268,9 @@ int workspace(int device, Workspace*& out) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace),
                                                       w.trace_threads, 0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
+        if (TV_COLD_GLOBAL)
+            TV_CK(cudaMalloc(&w.cold, static_cast<size_t>(w.trace_blocks) * w.trace_threads * kColdBytes),
+                  "cold state alloc");
         if (env_int("TV_VERBOSE", 0))
             std::fprintf(stderr, "tetvol_b200: trace kernel maxreg=%d threads=%d, %d blocks/SM resident, %d blocks\n",
                          maxreg, w.trace_threads, per_sm, w.trace_blocks);
@@ -329,6 +333,7 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.scatter_min = w.scatter_min;
         B.order = w.order;
         B.tile_order = tile_order;
+        B.cold = w.cold;
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
         TV_CK(cudaEventRecord(ev[0], st), "event");
         start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);

@@ -329,6 +329,8 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
         const size_t smem = mode == 0 ? trace_smem : 0;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(replay_kernel), 128, smem);
+        if (const char* v = std::getenv("TV_DIAG_BLOCKS"))  // what-if: cap the resident blocks per SM
+            if (mode == 0 && std::atoi(v) > 0) per_sm = std::min(per_sm, std::atoi(v));
         warps[mode] = per_sm * 4;
         const unsigned blocks = static_cast<unsigned>(sms * std::max(per_sm, 1));
         for (int r = 0; r < std::max(reps, 1); ++r) {

@@ -14,6 +14,10 @@ constexpr int kTraceThreads = TV_TRACE_THREADS;
 constexpr uint32_t kChunk = 64;               // paths a warp claims per queue atomic
 constexpr uint32_t kInvalidPixel = 0xfffffffeu;
 constexpr uint64_t kMaxBatchPaths = 1ull << 26;
+constexpr uint32_t kColdBytes = 6 * 8 + 8 + 3 * 4;  // cold path state per trace thread and path slot
+#ifndef TV_COLD_GLOBAL
+#define TV_COLD_GLOBAL 0  // cold path state in shared memory (see tv_path.inc)
+#endif
 
 // One render batch: this rank's pixels x samples [s0, s0 + ns).
 // Path index p -> unit = p / (ns * 32), s = s0 + (p / 32) % ns, lane = p % 32;
@@ -29,6 +33,7 @@ struct Batch {
     uint32_t regen_min, scatter_min;  // warp-batching thresholds of the trace loop
     uint32_t order;                   // path id order (see path_id in tv_trace.cu)
     const uint32_t* tile_order;       // this rank's tiles in processing order (null: t = rank + k * n_ranks)
+    void* cold;                       // trace kernel: cold path state (TV_COLD_GLOBAL), kColdBytes per thread
 };
 
 struct StartRec {  // camera ray of one path after TetMarcher::start
