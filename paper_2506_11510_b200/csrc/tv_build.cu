@@ -995,6 +995,8 @@ struct Buf {
     void reset() {
         if (!p) return;
         cudaStreamSynchronize(0);  // build kernels run on the legacy stream
+        static const bool verbose = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
+        const auto t0 = std::chrono::steady_clock::now();
         if (mapped) {
             const VmmApi& a = vmm();
             a.unmap(va, bytes);
@@ -1003,6 +1005,9 @@ struct Buf {
         } else {
             cudaFree(p);
         }
+        if (verbose && bytes >= (256u << 20))
+            std::fprintf(stderr, "tetvol_b200: build free %.1f MB: %.2f ms\n", bytes / 1048576.0,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         p = nullptr, bytes = 0, va = 0, reserved = 0, mapped = false;
         handles.clear();
     }
