@@ -165,6 +165,7 @@ struct Workspace {
     TraceFn trace = nullptr;
     int trace_threads = kTraceThreads;
     uint32_t regen_min = 8, scatter_min = 8, order = 0;
+    uint32_t tail_chunk = kChunk, tail_warps_x = 2;  // tail claims: size, and the zone in chunks per warp
     std::vector<cudaEvent_t> tev;  // per-batch kernel boundaries of the last frame (4 per batch)
     int n_timed = 0, n_launches = 0;
     // per (tiles_x, tiles_y, rank, n_ranks): that rank's tiles in processing
@@ -259,6 +260,8 @@ int workspace(int device, Workspace*& out) {
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 5));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 2));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
+        w.tail_chunk = static_cast<uint32_t>(std::min(std::max(env_int("TV_TAIL_CHUNK", 64), 1), 64));
+        w.tail_warps_x = static_cast<uint32_t>(std::max(env_int("TV_TAIL_ZONE", 2), 0));
         w.tile_mode = env_int("TV_TILE_ORDER", 1);
         w.tile_radius = env_int("TV_TILE_RADIUS_PCT", 80) / 100.0;
         int per_sm = 1;
@@ -334,6 +337,12 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.order = w.order;
         B.tile_order = tile_order;
         B.cold = w.cold;
+        {
+            // the last tail_warps_x chunks per resident warp are claimed tail_chunk at a time
+            const uint64_t zone = static_cast<uint64_t>(w.trace_blocks) * (w.trace_threads / 32) * kChunk * w.tail_warps_x;
+            B.tail_chunk = w.tail_chunk;
+            B.tail_from = B.n_paths > zone ? static_cast<uint32_t>(B.n_paths - zone) : 0u;
+        }
         const unsigned sb = static_cast<unsigned>(std::min<uint64_t>((B.n_paths + 255) / 256, w.sms * 16ull));
         TV_CK(cudaEventRecord(ev[0], st), "event");
         start_kernel<<<sb, 256, 0, st>>>(g.view, cv, rp, B, st_rec, cells);

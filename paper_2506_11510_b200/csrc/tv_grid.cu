@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <cstring>
+#include <cstdlib>
 #include <vector>
 
 #include "tv_trace.cuh"
@@ -154,8 +155,9 @@ __global__ void nodes_kernel(const tv_tet* __restrict__ tets, const uint4* __res
     out[tet2node[t]] = r;
 }
 
-__global__ void roots_kernel(const tv_tet* __restrict__ tets, const uint32_t* roots, const uint32_t* tet2leaf,
-                             const uint32_t* tet2node, uint32_t* out /* 24 ptr, 24 nid, 96 vid */) {
+__global__ void roots_kernel(const tv_tet* __restrict__ tets, const uint4* __restrict__ verts, const uint32_t* roots,
+                             const uint32_t* tet2leaf, const uint32_t* tet2node,
+                             uint32_t* out /* 24 ptr, 24 nid, 96 vid, 24 outer-face masks */) {
     const int r = threadIdx.x;
     if (r >= 24) return;
     const tv_tet& tt = tets[roots[r]];
@@ -163,6 +165,22 @@ __global__ void roots_kernel(const tv_tet* __restrict__ tets, const uint32_t* ro
     out[24 + r] = tt.normal_ids[0] | tt.normal_ids[1] << 8 | tt.normal_ids[2] << 16 |
                   static_cast<uint32_t>(tt.normal_ids[3]) << 24;
     for (int k = 0; k < 4; ++k) out[48 + 4 * r + k] = tt.verts[k];
+    // face f (opposite verts[f]) lies in a face of the unit cube when its three
+    // vertices share a coordinate of 0 or 2^24
+    uint32_t outer = 0;
+    for (int f = 0; f < 4; ++f) {
+        uint4 q[3];
+        int m = 0;
+        for (int k = 0; k < 4; ++k)
+            if (k != f) q[m++] = verts[tt.verts[k]];
+        for (int a = 0; a < 3; ++a) {
+            const uint32_t c0 = a == 0 ? q[0].x : (a == 1 ? q[0].y : q[0].z);
+            const uint32_t c1 = a == 0 ? q[1].x : (a == 1 ? q[1].y : q[1].z);
+            const uint32_t c2 = a == 0 ? q[2].x : (a == 1 ? q[2].y : q[2].z);
+            if (c0 == c1 && c1 == c2 && (c0 == 0u || c0 == (1u << 24))) outer |= 1u << f;
+        }
+    }
+    out[144 + r] = outer;
 }
 
 template <class T>
@@ -178,6 +196,60 @@ inline unsigned blocks(uint64_t n, unsigned t) { return static_cast<unsigned>((n
 
 }  // namespace
 
+// The locate jump table (GridView::jump): for cube c of a res^3 grid over the
+// unit cube, the deepest tree node whose tet contains all 8 corners of c
+// strictly — the root test with locate's 1e-9 interior margin, each descent
+// test with |dot(n, corner - pm)| > 1e-9 |n| on the same side for all corners —
+// or kNone when no root does. Corners are exact dyadic (i / res), so the only
+// rounding is in the dot products, ~1e-15 |n|: every point of the closed cube
+// takes the same branch at each of these levels in the reference's descent
+// (tet_grid.cpp:435-470), which is what lets locate start at the table's node.
+__global__ void jump_kernel(GridView G, int res, uint32_t* jump) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n = static_cast<uint32_t>(res) * res * res;
+    if (c >= n) return;
+    const int ix = static_cast<int>(c % res), iy = static_cast<int>((c / res) % res), iz = static_cast<int>(c / (res * res));
+    d3 corner[8];
+    for (int k = 0; k < 8; ++k)
+        corner[k] = mk(static_cast<double>(ix + (k & 1)) / res, static_cast<double>(iy + ((k >> 1) & 1)) / res,
+                       static_cast<double>(iz + (k >> 2)) / res);
+    uint32_t cur = kNone;
+    for (int r = 0; r < 24 && cur == kNone; ++r) {
+        // locate's root fast path, for every corner (the cube's points lie in
+        // the convex hull of its corners, and the violations are convex)
+        bool inside = true;
+        for (int k = 0; k < 8 && inside; ++k) {
+            double vi, vo;
+            root_violation2(G, r, corner[k], vi, vo);
+            inside = vi <= -1e-9 && vo <= 1e-12;
+        }
+        if (inside) cur = G.root_ptr[r];
+    }
+    if (cur == kNone) {
+        jump[c] = kNone;
+        return;
+    }
+    while (!(cur & kLeafBit)) {
+        const NodeRec& nd = G.nodes[cur];
+        const d3 nn = mk(nd.n[0], nd.n[1], nd.n[2]);
+        const d3 pm = mk(nd.pm[0], nd.pm[1], nd.pm[2]);
+        const double margin = 1e-9 * sqrt(dot(nn, nn));
+        bool all_a = true, all_b = true;
+        for (int k = 0; k < 8; ++k) {
+            const double sp = dot(nn, sub(corner[k], pm));
+            // child A holds sp >= 0 (sref_pos) or sp <= 0; demand a strict margin
+            const bool a = nd.sref_pos ? sp > margin : sp < -margin;
+            const bool b = nd.sref_pos ? sp < -margin : sp > margin;
+            all_a &= a;
+            all_b &= b;
+        }
+        if (all_a) cur = nd.child[0];
+        else if (all_b) cur = nd.child[1];
+        else break;
+    }
+    jump[c] = cur;
+}
+
 int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     const uint64_t nt = g.n_tets;
     int rc;
@@ -188,7 +260,7 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     int* d_depth = nullptr;
     void* temp = nullptr;
     size_t temp_bytes = 0, t1 = 0, t2 = 0;
-    std::vector<uint32_t> hroot(24 + 24 + 96);
+    std::vector<uint32_t> hroot(24 + 24 + 96 + 24);
 
     auto cleanup = [&]() {
         cudaFree(keys), cudaFree(keys_sorted), cudaFree(ids), cudaFree(order), cudaFree(is_int);
@@ -216,7 +288,7 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     TRY(dalloc(&is_int, nt, scratch_bytes));
     TRY(dalloc(&tet2node, nt, scratch_bytes));
     TRY(dalloc(&tet2leaf, nt, scratch_bytes));
-    TRY(dalloc(&rootbuf, 24 + 24 + 96, scratch_bytes));
+    TRY(dalloc(&rootbuf, 24 + 24 + 96 + 24, scratch_bytes));
     TRY(dalloc(&d_roots, 24, scratch_bytes));
     TRY(dalloc(&d_depth, 1, scratch_bytes));
 
@@ -247,7 +319,7 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     nodes_kernel<<<blocks(nt, 256), 256, 0, st>>>(g.tets, g.verts, nt, tet2leaf, tet2node, g.nodes);
     CK(cudaGetLastError(), "nodes_kernel");
     CK(cudaMemcpyAsync(d_roots, g.roots, sizeof(g.roots), cudaMemcpyHostToDevice, st), "roots H2D");
-    roots_kernel<<<1, 32, 0, st>>>(g.tets, d_roots, tet2leaf, tet2node, rootbuf);
+    roots_kernel<<<1, 32, 0, st>>>(g.tets, g.verts, d_roots, tet2leaf, tet2node, rootbuf);
     CK(cudaGetLastError(), "roots_kernel");
     CK(cudaMemcpyAsync(hroot.data(), rootbuf, hroot.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st),
        "roots D2H");
@@ -266,9 +338,27 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
         v.root_ptr[r] = hroot[r];
         v.root_nid[r] = hroot[24 + r];
         for (int k = 0; k < 4; ++k) v.root_vid[r][k] = hroot[48 + 4 * r + k];
+        v.root_outer[r] = hroot[144 + r];
     }
     v.n_leaves = static_cast<uint32_t>(g.n_leaves);
     v.n_nodes = static_cast<uint32_t>(g.n_internal);
+    v.jump = nullptr;
+    v.jump_res = 0;
+    {
+        // TV_JUMP_RES: cubes per axis of the locate jump table (0 = none);
+        // 128^3 entries = 8 MB
+        const char* e = std::getenv("TV_JUMP_RES");
+        const int res = e && *e ? std::atoi(e) : 128;
+        if (res > 0 && res <= 512) {
+            const uint32_t n = static_cast<uint32_t>(res) * res * res;
+            TRY(dalloc(&g.jump, n, g.bytes));
+            jump_kernel<<<blocks(n, 128), 128, 0, st>>>(v, res, g.jump);
+            CK(cudaGetLastError(), "jump_kernel");
+            CK(cudaStreamSynchronize(st), "jump table");
+            v.jump = g.jump;
+            v.jump_res = res;
+        }
+    }
     cleanup();
     return TV_OK;
 #undef CK
@@ -282,6 +372,8 @@ void free_grid(DeviceGrid& g) {
     cudaFree(g.nodes);
     cudaFree(g.leaf2tet);
     cudaFree(g.mask);
+    cudaFree(g.jump);
+    g.jump = nullptr;
     g.mask = nullptr;
     g.tets = nullptr;
     g.verts = nullptr;

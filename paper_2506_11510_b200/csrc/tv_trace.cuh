@@ -31,6 +31,8 @@ struct Batch {
     uint32_t n_paths;
     uint32_t first;  // 1 for the first batch of a frame (accumulators start at 0)
     uint32_t regen_min, scatter_min;  // warp-batching thresholds of the trace loop
+    uint32_t tail_chunk;              // paths per queue claim once the queue is nearly drained (<= kChunk)
+    uint32_t tail_from;               // queue position where the tail claims start
     uint32_t order;                   // path id order (see path_id in tv_trace.cu)
     const uint32_t* tile_order;       // this rank's tiles in processing order (null: t = rank + k * n_ranks)
     void* cold;                       // trace kernel: cold path state (TV_COLD_GLOBAL), kColdBytes per thread
@@ -81,6 +83,7 @@ struct DeviceGrid {
     NodeRec* nodes = nullptr;
     uint32_t* leaf2tet = nullptr;
     uint8_t* mask = nullptr;
+    uint32_t* jump = nullptr;  // locate jump table (view.jump)
     GridView view{};
     uint64_t bytes = 0;
 };

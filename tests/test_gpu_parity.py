@@ -113,6 +113,35 @@ def test_locate_points(tv, c1):
     assert np.array_equal(got, want)
 
 
+def test_locate_points_on_jump_table_boundaries(tv, c1):
+    """locate starts at the jump table's node (GridView::jump, 128^3 cubes) or
+    at the guessed root: points on the cube boundaries of that table (i / 128),
+    on the leaves' own vertices, just off them (+-1 ulp, +-1e-12), and on the
+    faces of the unit cube land in the reference's leaf."""
+    _, g, dg = c1
+    rng = np.random.default_rng(11)
+    n = 6000
+    pts = np.round(rng.random((n, 3)) * 128) / 128  # jump-table cube corners / edges / faces
+    pts[:1000, 0] = rng.random(1000)
+    verts = np.asarray(g.pools().vq, dtype=np.float64) / 2.0 ** 24
+    vi = rng.integers(0, len(verts), 2000)
+    pts[1000:3000] = verts[vi]
+    pts[3000:4000] = np.nextafter(pts[3000:4000], 2.0)
+    pts[4000:5000] = np.nextafter(pts[4000:5000], -1.0)
+    pts[5000:6000] = np.clip(pts[5000:6000] + rng.choice([-1e-12, 1e-12], (1000, 3)), 0.0, 1.0)
+    pts = np.clip(pts, 0.0, 1.0)
+    # points on the faces of the unit cube, where every camera ray enters (locate's
+    # root fast path accepts the root's outer face at violation 0)
+    face = rng.random((4000, 3))
+    ax = rng.integers(0, 3, 4000)
+    face[np.arange(4000), ax] = rng.integers(0, 2, 4000).astype(np.float64)
+    face[:500] = np.round(face[:500] * 64) / 64  # cube-face points on pyramid and triangle edges
+    pts = np.concatenate([pts, face])
+    got = tv.locate_points(dg, pts)
+    want = np.array([g.locate(p) for p in pts], dtype=np.uint32)
+    assert np.array_equal(got, want)
+
+
 def _render_both(tv, g, dg, cam_kw, rc_kw):
     cam = O.camera(**cam_kw)
     rc = O.render_cfg(**rc_kw)

@@ -1,5 +1,6 @@
 """Every selectable trace-kernel configuration (register cap, block size,
-warp-batching thresholds, path order; DESIGN.md §4 tuning knobs) renders the
+warp-batching thresholds, path order, locate jump-table resolution; DESIGN.md
+§4 tuning knobs) renders the
 same framebuffer bits: the knobs change scheduling, never results. Each
 configuration runs in a subprocess because the library reads the knobs once
 per process."""
@@ -25,6 +26,9 @@ CONFIGS = [
     {"TV_CARVEOUT": "50"},
     {"TV_TILE_ORDER": "2"},
     {"TV_TILE_ORDER": "2", "TV_TILE_RADIUS_PCT": "30"},
+    {"TV_JUMP_RES": "0"},
+    {"TV_JUMP_RES": "32"},
+    {"TV_JUMP_RES": "256"},
 ]
 
 
