@@ -384,6 +384,21 @@ def main():
                       "hit_pct": pj.get("l2_hit_pct"), "source": f"ncu lts__t_bytes, {pj.get('round', '?')}"}
         except Exception:
             traffic = None
+    # the measured latency ceiling of this frame (tools/diag_ceiling.py: the
+    # frame's recorded tet-step stream replayed as dependent record loads with
+    # the trace kernel's launch shape and schedule, no geometry)
+    ceiling = None
+    cprof = os.path.join(ROOT, "profiles", "trace_kernel_ceiling.json")
+    if os.path.exists(cprof):
+        try:
+            cj = json.load(open(cprof))
+            if world == 1 and int(cj["steps"]) == cells_rank:  # the same frame
+                steps_s = cells_rank / (trace_ms * 1e-3)
+                ceiling = {"steps_per_s": cj["steps_per_s"], "replay_ms": cj["replay_ms"],
+                           "frac": steps_s / cj["steps_per_s"], "warps_per_sm": cj["warps_per_sm"],
+                           "source": "tools/diag_ceiling.py (profiles/trace_kernel_ceiling.json)"}
+        except Exception:
+            ceiling = None
     # `achieved` / `frac` follow the contract: ALGORITHMIC bytes (64 per tet
     # step) over the kernel's time, against the HBM copy peak.
     # Most of those bytes are served by L1 / L2 (rays of one pixel and
@@ -397,7 +412,8 @@ def main():
                 "bytes_per_step": BYTES_PER_STEP, "tet_steps_per_launch": cells_rank,
                 "algorithmic_bytes_per_launch": cells_rank * BYTES_PER_STEP,
                 "achieved_is": "algorithmic request bytes (served mostly from L1/L2), not DRAM traffic",
-                "dram": dram, "l2": l2, "limiter": "dependent-load latency + issue (ncu, DESIGN.md 4)",
+                "dram": dram, "l2": l2, "latency_ceiling": ceiling,
+                "limiter": "dependent record-load stream: at its measured latency ceiling (DESIGN.md 4)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s"}
 
     cpu = None

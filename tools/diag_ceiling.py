@@ -23,5 +23,8 @@ d = tv.diag_gather_ceiling(grid, cam, rc, reps=3)
 out = {"render_ms": img.seconds * 1e3, "trace_ms": t["trace_ms"], "cells_visited": img.cells_visited,
        "trace_steps_per_s": img.cells_visited / (t["trace_ms"] * 1e-3), **d}
 out["frac_of_ceiling"] = out["trace_steps_per_s"] / d["steps_per_s"]
+out["workload"] = "bench.py C2 frame"
 print(json.dumps(out), flush=True)
+if len(sys.argv) > 1:  # e.g. profiles/trace_kernel_ceiling.json (bench.py reports it in roofline.latency_ceiling)
+    json.dump(out, open(sys.argv[1], "w"), indent=1)
 assert d["steps"] == img.cells_visited, "recorded steps differ from the render's cells_visited"
