@@ -272,10 +272,24 @@ __device__ __forceinline__ void stats_atomic(Stats& s, const Agg& a, bool with_t
     }
 }
 
-// global fire-and-forget atomics (RED; f64 adds are native in L2, where
-// shared-memory f64 adds would be CAS loops)
-__device__ __forceinline__ void stats_atomic_at(Stats* st, uint32_t owner, const Agg& a, bool with_tl) {
-    stats_atomic(st[owner], a, with_tl);
+// Where a voxel sweep adds its aggregates: global fire-and-forget atomics
+// (RED; f64 adds are native in L2, where shared-memory f64 adds would be CAS
+// loops). In the first rounds the owners are few (24 roots, then 48, 96, ...)
+// and every SM would hammer the same handful of L2 lines, so owners in
+// [lo, lo + n) are striped: lane l adds to stripe[(owner - lo) * 32 + l], and
+// stripe_combine_kernel folds the 32 stripes into the owner's Stats afterwards
+// (the order of the sums is free, as everywhere in the sweep).
+struct StatsSink {
+    Stats* st;
+    Stats* stripe;
+    uint32_t lo, n;  // striped owners; n = 0: none
+};
+constexpr uint32_t kStripes = 32;
+
+__device__ __forceinline__ void stats_atomic_at(const StatsSink& S, uint32_t owner, const Agg& a, bool with_tl) {
+    const uint32_t r = owner - S.lo;
+    if (r < S.n) stats_atomic(S.stripe[r * kStripes + (threadIdx.x & 31)], a, with_tl);
+    else stats_atomic(S.st[owner], a, with_tl);
 }
 
 __device__ __forceinline__ double wsum(double v) {
@@ -285,7 +299,7 @@ __device__ __forceinline__ double wsum(double v) {
 }
 
 // warp-synchronous flush of every lane's (cur, a) with has = a.cnt > 0
-__device__ __forceinline__ void warp_flush(Stats* st, uint32_t cur, Agg& a, bool with_tl) {
+__device__ __forceinline__ void warp_flush(const StatsSink& st, uint32_t cur, Agg& a, bool with_tl) {
     const bool has = a.cnt > 0;
     const unsigned m = __ballot_sync(0xffffffffu, has);
     if (!m) return;
@@ -313,6 +327,31 @@ __device__ __forceinline__ void warp_flush(Stats* st, uint32_t cur, Agg& a, bool
         stats_atomic_at(st, cur, a, with_tl);
     }
     agg_reset(a);
+}
+
+__global__ void stripe_zero_kernel(Stats* stripe, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Stats z;
+    z.sum = z.asum = z.tsum = z.tasum = z.lsum = z.lasum = 0.0;
+    z.cnt = 0, z.mn = 0xffffffffu, z.mx = 0u, z.pad = 0;
+    stripe[i] = z;
+}
+
+// fold owner lo + i's 32 stripes into its Stats (which the sweep left untouched)
+__global__ void stripe_combine_kernel(const Stats* stripe, uint32_t lo, uint32_t n, Stats* st) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Stats& t = st[lo + i];
+    for (uint32_t k = 0; k < kStripes; ++k) {
+        const Stats& z = stripe[i * kStripes + k];
+        if (!z.cnt) continue;
+        t.sum += z.sum, t.asum += z.asum, t.tsum += z.tsum, t.tasum += z.tasum, t.lsum += z.lsum,
+            t.lasum += z.lasum;
+        t.cnt += z.cnt;
+        t.mn = min(t.mn, z.mn);
+        t.mx = max(t.mx, z.mx);
+    }
 }
 
 // root of voxel centre p (tet_grid.cpp:435-451): the root whose pyramid and
@@ -361,10 +400,8 @@ __device__ __forceinline__ uint32_t descend(const NodeRec* split, const uint8_t*
 }
 
 // Sweep order: the volume is read as a flat array in groups of four voxels
-// (one 16-B owner load, one 16-B density load); lane l of a warp takes the
-// kVoxLaneGroups consecutive groups starting at group kVoxLaneGroups * l of
-// the warp's chunk, so a lane's voxels are contiguous (its owner changes only
-// at tet boundaries) and the warp's chunk is one contiguous span.
+// (one 16-B owner load, one 16-B density load); a warp's chunk is 32 *
+// kVoxLaneGroups consecutive groups (one contiguous span).
 constexpr int kVoxLaneGroups = 4;  // 16 voxels per lane, 512 per warp chunk
 
 struct VoxLane {
@@ -372,7 +409,7 @@ struct VoxLane {
     Agg a;
 };
 
-__device__ __forceinline__ void vox_add(Stats* st, VoxLane& L, uint32_t o, float x, const VolView& V,
+__device__ __forceinline__ void vox_add(const StatsSink& st, VoxLane& L, uint32_t o, float x, const VolView& V,
                                         uint64_t idx, bool with_tl) {
     if (o != L.cur) {
         if (L.a.cnt) stats_atomic_at(st, L.cur, L.a, with_tl);
@@ -398,9 +435,10 @@ __device__ __forceinline__ void vox_add(Stats* st, VoxLane& L, uint32_t o, float
     }
 }
 
-__global__ void __launch_bounds__(kVoxThreads) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
+template <int mode>
+__global__ void __launch_bounds__(kVoxThreads, 3) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
                                                                  const NodeRec* split, const uint8_t* flags,
-                                                                 uint32_t* owner, Stats* st, int mode, int with_tl) {
+                                                                 uint32_t* owner, StatsSink st, int with_tl) {
     const uint64_t nvox = static_cast<uint64_t>(V.nx) * V.ny * V.nz;
     const uint64_t n4 = nvox / 4;
     const int lane = threadIdx.x & 31;
@@ -409,13 +447,70 @@ __global__ void __launch_bounds__(kVoxThreads) vox_stats_kernel(VolView V, RootS
     const uint64_t per_warp = 32ull * kVoxLaneGroups;
     uint4* own4 = reinterpret_cast<uint4*>(owner);
     const float4* d4p = reinterpret_cast<const float4*>(V.dens);
+    // Groups are interleaved over the lanes (group q * 32 + lane of the warp's
+    // chunk), so every 16-B owner / density load of the warp is coalesced.
+    // kVoxDescend: the voxels to process (owner bisected) are a sparse, ragged
+    // subset of each chunk; unless most of the chunk is dirty they are first
+    // compacted per warp (shared memory, voxel order kept) and split into equal
+    // contiguous slices, one per lane: every lane descends and accumulates the
+    // same number of voxels, and a lane's voxels stay contiguous, so its owner
+    // runs survive. Dense chunks take the same vectorised path as the other modes.
+    __shared__ uint32_t s_pick[mode == kVoxDescend ? kVoxThreads / 32 : 1][32 * 4 * kVoxLaneGroups];
     for (uint64_t c = warp * per_warp; c < n4; c += n_warps * per_warp) {
         VoxLane L;
         agg_reset(L.a);
+        uint32_t dirty = 0xffffffffu;  // bit 4q + k: voxel k of this lane's group q is to be processed
+        if (mode == kVoxDescend) {
+            dirty = 0;
+#pragma unroll
+            for (int q = 0; q < kVoxLaneGroups; ++q) {
+                const uint64_t g = c + static_cast<uint64_t>(q) * 32 + lane;
+                if (g < n4) {
+                    const uint4 o4 = own4[g];
+                    // voxels whose owner is still a leaf keep it and were counted
+                    // when it was evaluated: skip them (no density read)
+                    dirty |= ((!(flags[o4.x] & F_LEAF) ? 1u : 0u) | (!(flags[o4.y] & F_LEAF) ? 2u : 0u) |
+                              (!(flags[o4.z] & F_LEAF) ? 4u : 0u) | (!(flags[o4.w] & F_LEAF) ? 8u : 0u))
+                             << (4 * q);
+                }
+            }
+            const uint32_t total = __reduce_add_sync(0xffffffffu, __popc(dirty));
+            if (total * 4 <= 3 * 32 * 4 * kVoxLaneGroups) {  // sparse: compact, then equal slices
+                uint32_t* pick = s_pick[threadIdx.x >> 5];
+                uint32_t base = 0;
+#pragma unroll
+                for (int q = 0; q < kVoxLaneGroups; ++q) {
+                    const uint32_t dq = (dirty >> (4 * q)) & 15u;
+                    const uint32_t cnt = __popc(dq);
+                    uint32_t pre = cnt;  // inclusive prefix over the lanes (voxel order within q)
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t v = __shfl_up_sync(0xffffffffu, pre, o);
+                        if (lane >= o) pre += v;
+                    }
+                    uint32_t at = base + pre - cnt;
+                    for (uint32_t b = dq; b; b &= b - 1)
+                        pick[at++] = (static_cast<uint32_t>(q) * 32 + lane) * 4 + __ffs(b) - 1;
+                    base += __shfl_sync(0xffffffffu, pre, 31);
+                }
+                __syncwarp();
+                const uint32_t lo = total * lane / 32, hi = total * (lane + 1) / 32;
+                for (uint32_t e = lo; e < hi; ++e) {
+                    const uint64_t idx = 4 * c + pick[e];
+                    const uint32_t o = descend(split, flags, owner[idx], voxel_centre(V, idx));
+                    owner[idx] = o;
+                    vox_add(st, L, o, V.dens[idx], V, idx, with_tl);
+                }
+                __syncwarp();
+                warp_flush(st, L.cur, L.a, with_tl);
+                continue;
+            }
+        }
 #pragma unroll 1
         for (int q = 0; q < kVoxLaneGroups; ++q) {
-            const uint64_t g = c + static_cast<uint64_t>(lane) * kVoxLaneGroups + q;
-            if (g >= n4) break;
+            const uint64_t g = c + static_cast<uint64_t>(q) * 32 + lane;
+            const uint32_t dq = (dirty >> (4 * q)) & 15u;
+            if (g >= n4 || !dq) continue;
             const uint64_t idx0 = 4 * g;
             uint4 o4;
             if (mode == kVoxInit) {
@@ -426,30 +521,19 @@ __global__ void __launch_bounds__(kVoxThreads) vox_stats_kernel(VolView V, RootS
                 own4[g] = o4;
             } else {
                 o4 = own4[g];
-                if (mode == kVoxDescend) {
-                    // voxels whose owner is still a leaf keep it and were counted
-                    // when it was evaluated: skip them (no density read)
-                    const bool l0 = flags[o4.x] & F_LEAF, l1 = flags[o4.y] & F_LEAF, l2 = flags[o4.z] & F_LEAF,
-                               l3 = flags[o4.w] & F_LEAF;
-                    if (l0 & l1 & l2 & l3) continue;
-                    const float4 d4 = d4p[g];
-                    if (!l0) vox_add(st, L, o4.x = descend(split, flags, o4.x, voxel_centre(V, idx0)), d4.x, V,
-                                     idx0, with_tl);
-                    if (!l1) vox_add(st, L, o4.y = descend(split, flags, o4.y, voxel_centre(V, idx0 + 1)), d4.y,
-                                     V, idx0 + 1, with_tl);
-                    if (!l2) vox_add(st, L, o4.z = descend(split, flags, o4.z, voxel_centre(V, idx0 + 2)), d4.z,
-                                     V, idx0 + 2, with_tl);
-                    if (!l3) vox_add(st, L, o4.w = descend(split, flags, o4.w, voxel_centre(V, idx0 + 3)), d4.w,
-                                     V, idx0 + 3, with_tl);
-                    own4[g] = o4;
-                    continue;
-                }
             }
             const float4 d4 = d4p[g];
-            vox_add(st, L, o4.x, d4.x, V, idx0, with_tl);
-            vox_add(st, L, o4.y, d4.y, V, idx0 + 1, with_tl);
-            vox_add(st, L, o4.z, d4.z, V, idx0 + 2, with_tl);
-            vox_add(st, L, o4.w, d4.w, V, idx0 + 3, with_tl);
+            if (mode == kVoxDescend) {  // dense chunk: descend the dirty voxels of the group
+                if (dq & 1u) o4.x = descend(split, flags, o4.x, voxel_centre(V, idx0));
+                if (dq & 2u) o4.y = descend(split, flags, o4.y, voxel_centre(V, idx0 + 1));
+                if (dq & 4u) o4.z = descend(split, flags, o4.z, voxel_centre(V, idx0 + 2));
+                if (dq & 8u) o4.w = descend(split, flags, o4.w, voxel_centre(V, idx0 + 3));
+                own4[g] = o4;
+            }
+            if (dq & 1u) vox_add(st, L, o4.x, d4.x, V, idx0, with_tl);
+            if (dq & 2u) vox_add(st, L, o4.y, d4.y, V, idx0 + 1, with_tl);
+            if (dq & 4u) vox_add(st, L, o4.z, d4.z, V, idx0 + 2, with_tl);
+            if (dq & 8u) vox_add(st, L, o4.w, d4.w, V, idx0 + 3, with_tl);
         }
         warp_flush(st, L.cur, L.a, with_tl);
     }
@@ -1302,6 +1386,9 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     uint64_t crit = 0, bisections = 0, passes = 0, replays = 0;
     int rounds = 0;
     uint32_t n_fresh = 24, n_marked = 0, n_leaves = 24;
+    uint32_t fresh_lo = 0;                    // the fresh leaves' ids lie in [fresh_lo, n_t)
+    constexpr uint32_t kStripeOwners = 32768;  // stripe up to 32K owners (64 MB of stripes)
+    Buf stripe_b;
     Buf fresh_b, marked_b;
     TRY(ensure(fresh_b, 24 * sizeof(uint32_t)));
     CK(cudaMemcpy(fresh_b.p, roots, sizeof(roots), cudaMemcpyHostToDevice), "fresh");
@@ -1334,9 +1421,24 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
                                                   flags_b.as<uint8_t>());
         // round 0: root scan of every voxel; later: descend the voxels whose
         // owner was bisected, skip the rest
-        vox_stats_kernel<<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
-                                                      flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
-                                                      stats_b.as<Stats>(), rounds == 0 ? kVoxInit : kVoxDescend, 0);
+        // this round's fresh leaves have ids in [fresh_lo, n_t): stripe their
+        // statistics while they are few (early rounds: hot atomics)
+        StatsSink sink{stats_b.as<Stats>(), nullptr, 0u, 0u};
+        const uint32_t fresh_range = n_t - fresh_lo;
+        if (fresh_range <= kStripeOwners) {
+            TRY(ensure(stripe_b, static_cast<size_t>(fresh_range) * kStripes * sizeof(Stats)));
+            stripe_zero_kernel<<<nblk(fresh_range * kStripes), 256>>>(stripe_b.as<Stats>(), fresh_range * kStripes);
+            sink = StatsSink{stats_b.as<Stats>(), stripe_b.as<Stats>(), fresh_lo, fresh_range};
+        }
+        if (rounds == 0)
+            vox_stats_kernel<kVoxInit><<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
+                                                                    flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
+                                                                    sink, 0);
+        else
+            vox_stats_kernel<kVoxDescend><<<vox_blocks, kVoxThreads>>>(
+                V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
+                sink, 0);
+        if (sink.n) stripe_combine_kernel<<<nblk(sink.n), 256>>>(sink.stripe, sink.lo, sink.n, stats_b.as<Stats>());
         CK(cudaGetLastError(), "voxel ownership");
         eval_kernel<<<nblk(n_fresh, 128), 128>>>(fresh_b.as<uint32_t>(), n_fresh, V, owner_b.as<uint32_t>(),
                                                   tets_b.as<tv_tet>(), verts_b.as<uint4>(), stats_b.as<Stats>(), E,
@@ -1353,6 +1455,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         if (n_marked == 0) break;
         crit += n_marked;
         ++rounds;
+        fresh_lo = n_t;  // every leaf the coming closure creates has an id >= fresh_lo
         // ---- closure ----
         double ph[4] = {0, 0, 0, 0};  // verbose: midpoint+dedup, bisect, leaves+hanging, select
         while (n_marked) {
@@ -1475,9 +1578,9 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     if (temp || alb) {
         stats_zero_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, stats_b.as<Stats>(),
                                                    flags_b.as<uint8_t>());
-        vox_stats_kernel<<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
-                                                      flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
-                                                      stats_b.as<Stats>(), kVoxAll, 1);
+        vox_stats_kernel<kVoxAll><<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
+                                                               flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
+                                                               StatsSink{stats_b.as<Stats>(), nullptr, 0u, 0u}, 1);
         CK(cudaGetLastError(), "voxel statistics");
     }
     PayloadParams PP{cfg->density_scale, temp != nullptr, alb != nullptr};
