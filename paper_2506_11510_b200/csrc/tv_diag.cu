@@ -122,11 +122,42 @@ __global__ void record_kernel(GridView G, CamView C, RenderParams P, Batch B, co
 // the trace kernel's warp schedule: idle lanes regenerate in batches
 // (regen_min), lanes whose flight collided wait for a scatter batch
 // (scatter_min), and the stepping lanes step until one changes state
+// What-if (TMA = true): each lane fetches its record with a 64-B bulk copy
+// (cp.async.bulk, the TMA unit: L2 -> shared memory, completion on a per-lane
+// mbarrier) and reads it from shared memory, so the L1 / LSU data pipe sees
+// only the shared-memory reads.
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load64(uint32_t dst, const void* src, uint32_t mbar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 64;" ::"r"(mbar) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 64, [%2];" ::"r"(dst),
+                 "l"(src), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(mbar),
+        "r"(phase)
+        : "memory");
+}
+
+template <bool TMA>
 __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t* __restrict__ start,
                               const uint32_t* __restrict__ counts, const uint32_t* __restrict__ codes,
                               const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t regen_min,
                               uint32_t scatter_min, uint32_t* counter, uint32_t* sink) {
     extern __shared__ uint32_t pad[];  // the render's shared-memory footprint (L1 split, blocks per SM)
+    __shared__ alignas(128) uint32_t rbuf[TMA ? 128 : 1][16];
+    __shared__ alignas(8) unsigned long long mbar[TMA ? 128 : 1];
+    uint32_t phase = 0;
+    if (TMA) {
+        mbar_init(static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x])), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncthreads();
+    }
     enum : int { IDLE = 0, STEP = 1, WAIT = 2 };
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
@@ -179,7 +210,21 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
         for (;;) {
             if (state == STEP) {
                 if ((k & 7) == 0) word = cw[k >> 3];
-                const LeafRec r = load_leaf(leaves, idx);
+                LeafRec r;
+                if (TMA) {
+                    const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
+                    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&rbuf[threadIdx.x][0]));
+                    bulk_load64(dst, leaves + idx, mb);
+                    mbar_wait(mb, phase);
+                    phase ^= 1u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(r.w[4 * q]), "=r"(r.w[4 * q + 1]), "=r"(r.w[4 * q + 2]), "=r"(r.w[4 * q + 3])
+                                     : "r"(dst + 16 * q));
+                } else {
+                    r = load_leaf(leaves, idx);
+                }
                 acc ^= r.w[5] ^ r.w[10] ^ r.w[15];
                 const uint32_t code = (word >> (4 * (k & 7))) & 15u;
                 ++k;
@@ -310,11 +355,12 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
                         sizeof(unsigned long long) * kTraceThreads + 3 * sizeof(uint32_t) * kTraceThreads;
     // what-if knobs (dev): shared-memory footprint per block and carveout of the first replay
     if (const char* v = std::getenv("TV_DIAG_SMEM")) trace_smem = static_cast<size_t>(std::atol(v));
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(replay_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(trace_smem));
+    const bool tma = std::getenv("TV_DIAG_TMA") && std::atoi(std::getenv("TV_DIAG_TMA")) > 0;
+    const void* rk = tma ? reinterpret_cast<const void*>(replay_kernel<true>)
+                         : reinterpret_cast<const void*>(replay_kernel<false>);
+    cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trace_smem));
     const char* cv_env = std::getenv("TV_DIAG_CARVEOUT") ? std::getenv("TV_DIAG_CARVEOUT") : std::getenv("TV_CARVEOUT");
-    cudaFuncSetAttribute(reinterpret_cast<const void*>(replay_kernel), cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cv_env && *cv_env ? std::atoi(cv_env) : 72);
+    cudaFuncSetAttribute(rk, cudaFuncAttributePreferredSharedMemoryCarveout, cv_env && *cv_env ? std::atoi(cv_env) : 72);
     auto env_u = [](const char* name, uint32_t d) {
         const char* v = std::getenv(name);
         return v && *v ? static_cast<uint32_t>(std::atoi(v)) : d;
@@ -328,7 +374,7 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
     for (int mode = 0; mode < 2; ++mode) {
         const size_t smem = mode == 0 ? trace_smem : 0;
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(replay_kernel), 128, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk, 128, smem);
         if (const char* v = std::getenv("TV_DIAG_BLOCKS"))  // what-if: cap the resident blocks per SM
             if (mode == 0 && std::atoi(v) > 0) per_sm = std::min(per_sm, std::atoi(v));
         warps[mode] = per_sm * 4;
@@ -336,7 +382,7 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
         for (int r = 0; r < std::max(reps, 1); ++r) {
             CK(cudaMemset(ctr.p, 0, 256), "diag");
             cudaEventRecord(e0);
-            replay_kernel<<<blocks, 128, smem>>>(g.leaves, static_cast<const uint32_t*>(cells.p),
+            (tma ? replay_kernel<true> : replay_kernel<false>)<<<blocks, 128, smem>>>(g.leaves, static_cast<const uint32_t*>(cells.p),
                                                  static_cast<const uint32_t*>(counts.p),
                                                  static_cast<const uint32_t*>(seq.p),
                                                  static_cast<const uint64_t*>(offs.p), B.n_paths, regen_min,
