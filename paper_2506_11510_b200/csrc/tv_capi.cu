@@ -171,11 +171,16 @@ struct Workspace {
     // per (tiles_x, tiles_y, rank, n_ranks): that rank's tiles in processing
     // order (see tile_order_for); written once, never overwritten, so frames
     // still in flight keep reading a valid table
-    std::map<TileOrderKey, uint32_t*> tile_orders;
+    struct TileTables {
+        uint32_t* order = nullptr;  // this rank's tiles in processing order
+        uint32_t* cost = nullptr;   // TV_TILE_ORDER=3: tet steps per list position in the last frame
+    };
+    std::map<TileOrderKey, TileTables> tile_orders;
     int tile_mode = 1;
     double tile_radius = 0.8;  // outer tiles: beyond this fraction of the inscribed circle
 };
 Workspace g_ws[64];
+constexpr uint32_t kSortTiles = 4096;  // TV_TILE_ORDER=3 sorts at most this many tiles per rank
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -188,18 +193,26 @@ int env_int(const char* name, int dflt) {
 // come last. Central tiles carry the long paths through the medium, so the
 // persistent trace kernel's last chunks are short paths and its tail shrinks.
 // Only the schedule changes: every pixel still accumulates its samples in
-// order. TV_TILE_ORDER: 0 raster always, 1 (default) from 4 ranks up, 2 always.
+// order. TV_TILE_ORDER: 0 raster always, 1 (default) from 4 ranks up, 2 always,
+// 3 cost-ordered from 4 ranks up, 4 cost-ordered always: the trace kernel adds
+// every path's tet steps to its tile's counter, and after each frame
+// tile_sort_kernel orders this rank's tiles by the last frame's cost, longest
+// first (ties by tile id), for the next frame; the first frame uses the order
+// of mode 2.
 int tile_order_for(Workspace& w, uint32_t tiles_x, uint32_t tiles_y, int rank, int n_ranks, cudaStream_t st,
-                   const uint32_t*& out) {
+                   const uint32_t*& out, uint32_t** cost = nullptr) {
     out = nullptr;
+    if (cost) *cost = nullptr;
     // measured on B200 (tools/rank_share.py, C2): the reordering shortens the
     // per-rank tail at 4 and 8 ranks (8.89 vs 9.13 ms per rank at 8) but costs
     // L2 locality on a full frame (+0.3 % at 1 and 2 ranks)
-    if (w.tile_mode == 0 || (w.tile_mode == 1 && n_ranks < 4)) return TV_OK;
+    if (w.tile_mode == 0 || ((w.tile_mode == 1 || w.tile_mode == 3) && n_ranks < 4)) return TV_OK;
+    const bool by_cost = w.tile_mode >= 3;
     const TileOrderKey key{{tiles_x, tiles_y, static_cast<uint32_t>(rank), static_cast<uint32_t>(n_ranks)}};
     auto it = w.tile_orders.find(key);
     if (it != w.tile_orders.end()) {
-        out = it->second;
+        out = it->second.order;
+        if (cost) *cost = it->second.cost;
         return TV_OK;
     }
     std::vector<uint32_t> tl;
@@ -217,20 +230,39 @@ int tile_order_for(Workspace& w, uint32_t tiles_x, uint32_t tiles_y, int rank, i
     std::stable_partition(tl.begin(), tl.end(), [&](uint32_t t) { return !outer(t); });
     if (w.tile_orders.size() >= 64) {  // bounded cache: drop the tables once nothing can read them
         TV_CK(cudaEventSynchronize(w.idle), "tile order sync");
-        for (auto& kv : w.tile_orders) cudaFree(kv.second);
+        for (auto& kv : w.tile_orders) cudaFree(kv.second.order), cudaFree(kv.second.cost);
         w.tile_orders.clear();
     }
-    uint32_t* d = nullptr;
-    TV_CK(cudaMalloc(&d, tl.size() * sizeof(uint32_t)), "tile order alloc");
+    Workspace::TileTables tt;
+    TV_CK(cudaMalloc(&tt.order, tl.size() * sizeof(uint32_t)), "tile order alloc");
     // stream-ordered upload (a pageable source is staged before the call returns)
-    const cudaError_t e = cudaMemcpyAsync(d, tl.data(), tl.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) {
-        cudaFree(d);
-        return cuda_status(e, "tile order H2D");
+    cudaError_t e = cudaMemcpyAsync(tt.order, tl.data(), tl.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && by_cost && tl.size() <= kSortTiles) {
+        e = cudaMalloc(&tt.cost, tl.size() * sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMemsetAsync(tt.cost, 0, tl.size() * sizeof(uint32_t), st);
     }
-    w.tile_orders.emplace(key, d);
-    out = d;
+    if (e != cudaSuccess) {
+        cudaFree(tt.order), cudaFree(tt.cost);
+        return cuda_status(e, "tile order tables");
+    }
+    w.tile_orders.emplace(key, tt);
+    out = tt.order;
+    if (cost) *cost = tt.cost;
     return TV_OK;
+}
+
+// TV_TILE_ORDER=3: this rank's tiles by the last frame's cost (tet steps),
+// descending, ties by tile id; resets the costs. One block, n <= kSortTiles.
+__global__ void tile_sort_kernel(uint32_t* order, uint32_t* cost, uint32_t n) {
+    __shared__ uint32_t sc[kSortTiles], st[kSortTiles];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sc[i] = cost[i], st[i] = order[i];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        uint32_t r = 0;
+        for (uint32_t j = 0; j < n; ++j) r += (sc[j] > sc[i]) || (sc[j] == sc[i] && st[j] < st[i]);
+        order[r] = st[i];
+        cost[i] = 0;
+    }
 }
 
 int grow(void*& p, size_t& have, size_t need, cudaEvent_t idle) {
@@ -300,7 +332,8 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
     // the previous frame on this device (any stream) is done with the workspace
     TV_CK(cudaStreamWaitEvent(st, w.idle, 0), "wait workspace");
     const uint32_t* tile_order = nullptr;
-    if (int rc = tile_order_for(w, tiles_x, tiles_y, rank, n_ranks, st, tile_order)) return rc;
+    uint32_t* tile_cost = nullptr;
+    if (int rc = tile_order_for(w, tiles_x, tiles_y, rank, n_ranks, st, tile_order, &tile_cost)) return rc;
     uint64_t ns = std::max<uint64_t>(1, kMaxBatchPaths / (units * 32));
     ns = std::min<uint64_t>(ns, static_cast<uint64_t>(rp.spp));
     if (units * 32 * ns >= (1ull << 31)) return set_error(TV_ERR_ARG, "frame too large for one batch");
@@ -336,6 +369,7 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.scatter_min = w.scatter_min;
         B.order = w.order;
         B.tile_order = tile_order;
+        B.tile_cost = tile_cost;
         B.cold = w.cold;
         {
             // the last tail_warps_x chunks per resident warp are claimed tail_chunk at a time
@@ -357,6 +391,12 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         accum_kernel<<<ab, 128, 0, st>>>(B, cv, cells, rad, out);
         TV_CK(cudaGetLastError(), "accum_kernel launch");
         TV_CK(cudaEventRecord(ev[3], st), "event");
+    }
+    if (tile_cost) {  // the next frame's order, after this frame's last accumulate read the current one
+        tile_sort_kernel<<<1, 1024, 0, st>>>(const_cast<uint32_t*>(tile_order), tile_cost,
+                                              static_cast<uint32_t>(mine));
+        TV_CK(cudaGetLastError(), "tile_sort_kernel launch");
+        ++w.n_launches;
     }
     TV_CK(cudaEventRecord(w.idle, st), "event");
     return TV_OK;

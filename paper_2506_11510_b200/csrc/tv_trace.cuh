@@ -36,6 +36,7 @@ struct Batch {
     uint32_t order;                   // path id order (see path_id in tv_trace.cu)
     const uint32_t* tile_order;       // this rank's tiles in processing order (null: t = rank + k * n_ranks)
     void* cold;                       // trace kernel: cold path state (TV_COLD_GLOBAL), kColdBytes per thread
+    uint32_t* tile_cost;              // TV_TILE_ORDER=3: tet steps per tile-list position (null: off)
 };
 
 struct StartRec {  // camera ray of one path after TetMarcher::start

@@ -21,5 +21,8 @@ p.tets["albedo"][leaf] = rng.random(leaf.sum()).astype(np.float32)
 p.tets["mask"][leaf] = 7
 dg = tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots, p.max_level)
 cam = tv.PinholeCamera((0.5, 0.5, -2), (0, 0, 1), (0, 1, 0), 40, 160, 120)
-img = tv.render(dg, cam, tv.RenderConfig(spp=16, max_bounces=64, seed=3, hg_g=0.4))
+rc = tv.RenderConfig(spp=16, max_bounces=64, seed=3, hg_g=0.4)
+img = tv.render(dg, cam, rc)
+img2 = tv.render(dg, cam, rc)  # a second frame: schedules that adapt between frames (TV_TILE_ORDER=4)
+assert O.fnv64(img2.sum) == O.fnv64(img.sum) and img2.cells_visited == img.cells_visited
 print(f"{O.fnv64(img.sum):016x} {O.fnv64(img.sum_sq):016x} {img.cells_visited}")

@@ -26,6 +26,7 @@ CONFIGS = [
     {"TV_CARVEOUT": "50"},
     {"TV_TILE_ORDER": "2"},
     {"TV_TILE_ORDER": "2", "TV_TILE_RADIUS_PCT": "30"},
+    {"TV_TILE_ORDER": "4"},
     {"TV_JUMP_RES": "0"},
     {"TV_JUMP_RES": "32"},
     {"TV_JUMP_RES": "256"},
