@@ -108,8 +108,42 @@ def warmup():
     g.close()
 
 
+
+
+def c3_shares():
+    """C3 as the BASELINE names it (1024 spp, sharded over 2/4/8 GPUs): the
+    slowest rank's share of the frame, rendered on this one GPU (rank 0 and
+    rank N-1), at the BASELINE threshold 0.15 and the paper-like 4.0."""
+    vol = field(512)
+    cam = tv.PinholeCamera(**CAM)
+    rc = tv.RenderConfig(spp=1024, max_bounces=64, seed=0)
+    s = torch.zeros(1024 * 1024 * 3, dtype=torch.float64, device="cuda")
+    q = torch.zeros_like(s)
+    c = torch.zeros(1024 * 1024, dtype=torch.int32, device="cuda")
+    st = torch.zeros(3, dtype=torch.int64, device="cuda")
+    for thr in [0.15, 4.0]:
+        g, _, _ = build(vol, 512, thr, 27)
+        for nr in (8, 4, 2):
+            worst = 0.0
+            cells = 0
+            for r in ([0, nr - 1]):
+                st.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                tv.render_tiles(g, cam, rc, r, nr, s.data_ptr(), q.data_ptr(), c.data_ptr(), st.data_ptr(), 0)
+                e1.record()
+                torch.cuda.synchronize()
+                worst = max(worst, e0.elapsed_time(e1))
+                cells = max(cells, int(st[0]))
+            row(config=f"C3 share (1024 spp, {nr} ranks)", field="cloud 512^3 + camera", threshold=thr,
+                leaves=g.info()["n_leaves"], slowest_rank_ms=worst,
+                frame_ms_at_n_gpus_render_only=worst, samples_per_s_whole_job=1024 * 1024 * 1024 / (worst * 1e-3),
+                rank_tet_steps=cells)
+        g.close()
+
+
 if __name__ == "__main__":
-    rows = sys.argv[1:] or ["c2", "c3", "c4"]
+    rows = sys.argv[1:] or ["c2", "c3", "c4"]  # also: c3shares
     warmup()
     if "c2" in rows:
         c2()
@@ -117,3 +151,5 @@ if __name__ == "__main__":
         c3_c5()
     if "c4" in rows:
         c4()
+    if "c3shares" in rows:
+        c3_shares()

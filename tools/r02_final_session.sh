@@ -1,4 +1,5 @@
 #!/bin/bash
+# Dev tool: the round-2 validation session (all GPU tests, smoke, bench, reference arm, profiles/ capture, C4 configs).
 cd $GRAFT_REPO_ROOT
 timeout 1800 python -m pytest -q -m gpu tests > gpurun_out/g28_tests.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/g28_smoke.log 2>&1
