@@ -141,3 +141,23 @@ def test_spot_rays_match_reference_cli():
         want = np.zeros((300, 8))
         ref.fn("spot_rays")(seed, 300, want.ctypes.data_as(C.POINTER(C.c_double)))
         assert np.array_equal(mine.view(np.uint64), want.view(np.uint64))
+
+
+def test_ipc_and_diag_entry_points_fail_loudly_without_a_gpu():
+    """The peer-write helpers and the diagnostic validate their arguments and,
+    without a device, return TV_ERR_CUDA / TV_ERR_ARG instead of doing anything."""
+    import ctypes as C
+
+    import paper_2506_11510_b200 as tv
+
+    lib = tv._lib
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64()
+    assert lib.tv_ipc_export(None, h, C.byref(off)) != 0  # null pointer
+    out = C.c_void_p()
+    rc = lib.tv_ipc_open(h, 0, 0, C.byref(out))
+    if tv.device_count() == 0:
+        assert rc == 6  # TV_ERR_CUDA: no device, no fallback
+    assert lib.tv_ipc_close(None, 0) == 0
+    res = (C.c_double * 6)()
+    assert lib.tv_diag_gather_ceiling(None, None, None, 1, res) == 8  # TV_ERR_ARG
