@@ -672,12 +672,19 @@ __global__ void eval_kernel(const uint32_t* list, uint32_t n, VolView V, const u
                             const uint4* verts, const Stats* st, EvalParams E, uint8_t* flags,
                             unsigned long long* counters /* [0] replays [1] voxel visits */) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    // voxel-visit count: one atomic per warp (a per-thread atomic on one
+    // counter serialises millions of leaves in L2)
+    {
+        unsigned long long c = i < n ? st[list[i]].cnt : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(counters + 1, c);
+    }
     if (i >= n) return;
     const uint32_t t = list[i];
     const tv_tet tt = tets[t];
     const Stats s = st[t];
     flags[t] &= static_cast<uint8_t>(~F_EVAL);
-    atomicAdd(counters + 1, static_cast<unsigned long long>(s.cnt));
     if (s.cnt == 0) return;  // trilinear fallback: min == max == mean -> variation 0
     const double nn = static_cast<double>(s.cnt);
     const double mn = unord_f(s.mn), mx = unord_f(s.mx);
@@ -727,8 +734,16 @@ __global__ void midpoint_kernel(const uint32_t* marked, uint32_t n, const tv_tet
                    mz = static_cast<uint32_t>(sz / 2);
     const uint32_t v = hash_find(table, mask, verts, mx, my, mz);
     mid_vid[i] = v;
+    // missing midpoints claim their slots with one atomic per warp
+    const unsigned act = __activemask();
+    const unsigned m = __ballot_sync(act, v == kNone);
+    if (!m) return;
+    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(n_miss, static_cast<uint32_t>(__popc(m)));
+    base = __shfl_sync(act, base, leader);
     if (v == kNone) {
-        const uint32_t k = atomicAdd(n_miss, 1u);
+        const uint32_t k = base + __popc(m & ((1u << lane) - 1u));
         miss_hi[k] = static_cast<uint64_t>(mx) << 25 | my;
         miss_lo[k] = mz;
         miss_idx[k] = i;
@@ -886,7 +901,10 @@ __global__ void payload_kernel(const uint32_t* list, uint32_t n, VolView V, cons
     const uint32_t t = list[i];
     tv_tet tt = tets[t];
     const Stats s = st[t];
-    atomicMax(max_depth, static_cast<int>(tt.level));
+    {  // one atomic per warp
+        const int lv = __reduce_max_sync(__activemask(), static_cast<int>(tt.level));
+        if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(__activemask()) - 1)) atomicMax(max_depth, lv);
+    }
     float dens, temp = 0.f, alb = 0.f;
     if (s.cnt == 0) {
         d3 c[4];

@@ -99,7 +99,9 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
     dst[1] = make_uint4(r.w[4], r.w[5], r.w[6], r.w[7]);
     dst[2] = make_uint4(r.w[8], r.w[9], r.w[10], r.w[11]);
     dst[3] = make_uint4(r.w[12], r.w[13], r.w[14], r.w[15]);
-    atomicMax(max_depth, static_cast<int>(tt.level));
+    const unsigned act = __activemask();  // one atomic per warp
+    const int lv = __reduce_max_sync(act, static_cast<int>(tt.level));
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(act) - 1)) atomicMax(max_depth, lv);
 }
 
 // tet_grid.cpp:288-330 (exact integer longest edge; ties towards smaller ids)
