@@ -776,7 +776,7 @@ __global__ void dedup_assign_kernel(const uint64_t* hi, const uint32_t* lo, cons
 // n_t + 2i, n_t + 2i + 1 in marked-list (ascending id) order.
 __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, tv_tet* tets, uint4* tv4,
                               const uint4* verts, const uint32_t* mid_vid, NodeRec* split, uint8_t* flags,
-                              uint8_t* vtouch, int max_level, int* err) {
+                              uint32_t* vtouch, int max_level, int* err) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t t = marked[i];
@@ -811,8 +811,10 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
     flags[ida] = F_LEAF | F_NEW;
     flags[idb] = F_LEAF | F_NEW;
     flags[t] = 0;
-    vtouch[parent.verts[s0]] = 1;
-    vtouch[parent.verts[s1]] = 1;
+    // touched vertices as a bitmask (1 bit per vertex: the hanging test's
+    // lookups stay in L1 / L2)
+    atomicOr(vtouch + (parent.verts[s0] >> 5), 1u << (parent.verts[s0] & 31));
+    atomicOr(vtouch + (parent.verts[s1] >> 5), 1u << (parent.verts[s1] & 31));
     // split plane for the owner-map descent (tet_grid.cpp:453-470)
     const d3 pm = vpos(verts[vm]);
     int oa = -1, ob = -1;
@@ -841,13 +843,16 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
 // bisected tet, whose two endpoints were touched).
 __global__ void hanging_kernel(uint32_t n_t, uint32_t first_new, const uint4* __restrict__ tv4,
                                const uint4* __restrict__ verts, const uint32_t* __restrict__ table, uint64_t mask,
-                               const uint8_t* __restrict__ vtouch, uint8_t* flags) {
+                               const uint32_t* __restrict__ vtouch, uint8_t* flags) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_t) return;
     const uint8_t f = flags[t];
     if (!(f & F_LEAF)) return;
     const uint4 tv = tv4[t];
-    if (t < first_new && vtouch[tv.x] + vtouch[tv.y] + vtouch[tv.z] + vtouch[tv.w] < 2) return;
+    if (t < first_new) {
+        auto bit = [&](uint32_t v) { return (__ldg(vtouch + (v >> 5)) >> (v & 31)) & 1u; };
+        if (bit(tv.x) + bit(tv.y) + bit(tv.z) + bit(tv.w) < 2) return;
+    }
     uint4 q[4] = {verts[tv.x], verts[tv.y], verts[tv.z], verts[tv.w]};
     for (int e = 0; e < 6; ++e) {
         const uint4 a = q[ep0(e)], b = q[ep1(e)];
@@ -1315,7 +1320,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         if (need <= cap_v) return TV_OK;
         const size_t nc = std::max(need, cap_v * 2 + 1024);
         TRY(ensure(verts_b, nc * sizeof(uint4), true));
-        TRY(ensure(vtouch_b, nc, true));
+        TRY(ensure(vtouch_b, (nc + 31) / 32 * 4, true));
         size_t slots = 1024;
         while (slots < 2 * nc) slots <<= 1;
         TRY(ensure(table_b, slots * sizeof(uint32_t)));
@@ -1542,11 +1547,11 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
                 CK(cudaGetLastError(), "dedup assign");
             }
             if (verbose) ph[0] += since(tp), tp = now();
-            CK(cudaMemset(vtouch_b.p, 0, n_v), "vtouch");  // bisect touches existing vertices only
+            CK(cudaMemset(vtouch_b.p, 0, (n_v + 31) / 32 * 4), "vtouch");  // bisect touches existing vertices only
             bisect_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, n_t, tets_b.as<tv_tet>(),
                                                    tv4_b.as<uint4>(), verts_b.as<uint4>(), mid_b.as<uint32_t>(),
                                                    split_b.as<NodeRec>(), flags_b.as<uint8_t>(),
-                                                   vtouch_b.as<uint8_t>(), grid_max_level, d_err);
+                                                   vtouch_b.as<uint32_t>(), grid_max_level, d_err);
             CK(cudaGetLastError(), "bisect");
             const uint32_t first_new = n_t;
             n_t += 2 * n_marked;
@@ -1555,7 +1560,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             if (verbose) ph[1] += since(tp), tp = now();
             // hanging test over every tet id, then the marked list (ascending ids)
             hanging_kernel<<<nblk(n_t), 256>>>(n_t, first_new, tv4_b.as<uint4>(), verts_b.as<uint4>(),
-                                               table_b.as<uint32_t>(), hmask, vtouch_b.as<uint8_t>(),
+                                               table_b.as<uint32_t>(), hmask, vtouch_b.as<uint32_t>(),
                                                flags_b.as<uint8_t>());
             CK(cudaGetLastError(), "hanging");
             if (verbose) ph[2] += since(tp), tp = now();
