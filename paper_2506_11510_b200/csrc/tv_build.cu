@@ -436,7 +436,7 @@ __device__ __forceinline__ void vox_add(const StatsSink& st, VoxLane& L, uint32_
 }
 
 template <int mode>
-__global__ void __launch_bounds__(kVoxThreads, 3) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
+__global__ void __launch_bounds__(kVoxThreads, mode == kVoxDescend ? 4 : 3) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
                                                                  const NodeRec* split, const uint8_t* flags,
                                                                  uint32_t* owner, StatsSink st, int with_tl) {
     const uint64_t nvox = static_cast<uint64_t>(V.nx) * V.ny * V.nz;
