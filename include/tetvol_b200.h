@@ -217,6 +217,14 @@ int tv_build(const float* density, const float* temperature, const float* albedo
 int tv_build_dev(const float* density_dev, const float* temperature_dev, const float* albedo_dev, int32_t nx,
                  int32_t ny, int32_t nz, const tv_build_config* cfg, const tv_camera* camera, int device,
                  tv_grid** out, tv_build_stats* stats);
+/* Build scratch (not in the reference, whose builder allocates on the host):
+ * the device buffers a build works in stay allocated on their device after
+ * the build and are reused by the next one, so warm builds do no driver
+ * allocation (TV_BUILD_CACHE=0 turns this off). tv_build_trim releases them
+ * (device -1: every device); tv_build_scratch_bytes reports what is held.
+ * A failed build releases its device's scratch itself. */
+int tv_build_trim(int device);
+uint64_t tv_build_scratch_bytes(int device);
 /* Procedural fields on the device (kind: 0 constant, 1 ramp, 2 blob, 3 step,
  * 4 noise, 5 cloud; cli.cpp:317-346). out_dev: nx*ny*nz f32. */
 int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, double value, float* out_dev,

@@ -158,6 +158,8 @@ _sig("tv_build", C.c_int, _F, _F, _F, C.c_int32, C.c_int32, C.c_int32, C.POINTER
      C.c_int, C.POINTER(_P), C.POINTER(_BuildStats))
 _sig("tv_build_dev", C.c_int, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_BuildConfig),
      C.POINTER(_Camera), C.c_int, C.POINTER(_P), C.POINTER(_BuildStats))
+_sig("tv_build_trim", C.c_int, C.c_int)
+_sig("tv_build_scratch_bytes", C.c_uint64, C.c_int)
 _sig("tv_generate_volume_dev", C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, C.c_int)
 _sig("tv_render", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.POINTER(_Framebuffer),
      C.POINTER(_RenderStats))
@@ -583,6 +585,16 @@ def build_adaptive_grid_dev(density_dev: int, shape, cfg: BuildConfig, camera: P
     return TetGrid(h), BuildStats(**{k: getattr(st, k) for k, _ in _BuildStats._fields_})
 
 
+def build_trim(device: int = -1) -> None:
+    """Release the build scratch kept on `device` (-1: all devices) for the next build."""
+    _check(_lib.tv_build_trim(int(device)))
+
+
+def build_scratch_bytes(device: int = -1) -> int:
+    """Device bytes of build scratch currently held (see tv_build_trim)."""
+    return int(_lib.tv_build_scratch_bytes(int(device)))
+
+
 VOLUME_KINDS = {"constant": 0, "ramp": 1, "blob": 2, "step": 3, "noise": 4, "cloud": 5}
 
 
@@ -651,7 +663,7 @@ __all__ = [
     "pfm_pixels", "read_pfm", "render_accumulate", "write_pfm", "write_variance_pfm",
     "ImageAccumulator", "IoError", "load_grid", "save_grid", "spot_rays",
     "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
-    "build_adaptive_grid", "build_adaptive_grid_dev", "device_count", "generate_volume_dev", "locate_points",
+    "build_adaptive_grid", "build_adaptive_grid_dev", "build_scratch_bytes", "build_trim", "device_count", "generate_volume_dev", "locate_points",
     "march_segments", "march_transmittance", "trace", "sample_free_path", "FREE_PATH_DTYPE", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",
     "tile_unpack", "version",
 ]

@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -1094,7 +1095,8 @@ struct Buf {
     CUdeviceptr va = 0;
     size_t reserved = 0;
     std::vector<CUmemGenericAllocationHandle> handles;
-    bool mapped = false;  // VMM-backed
+    std::vector<size_t> sizes;  // bytes of each handle, in mapping order
+    bool mapped = false;        // VMM-backed
     Buf() = default;
     Buf(const Buf&) = delete;
     Buf& operator=(const Buf&) = delete;
@@ -1117,6 +1119,7 @@ struct Buf {
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         p = nullptr, bytes = 0, va = 0, reserved = 0, mapped = false;
         handles.clear();
+        sizes.clear();
     }
     template <class T>
     T* as() {
@@ -1124,11 +1127,27 @@ struct Buf {
     }
 };
 
+// TV_BUILD_POISON=1 (tests): fill every scratch byte the build has not written with 0x5A (new
+// growth, and every cached buffer at the start of a build), so that a kernel reading memory it did
+// not initialise shows up as a parity failure instead of relying on zeroed fresh pages.
+bool poison() {
+    static const bool p = std::getenv("TV_BUILD_POISON") && std::atoi(std::getenv("TV_BUILD_POISON"));
+    return p;
+}
+
 // grow b to at least `bytes`, keeping its contents
 int ensure(Buf& b, size_t bytes, bool /*keep: contents are always kept*/ = false) {
     if (b.bytes >= bytes) return TV_OK;
     static const bool verbose = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 1;
+    static const bool verbose3 = std::getenv("TV_VERBOSE") && std::atoi(std::getenv("TV_VERBOSE")) > 2;
     const auto t0 = std::chrono::steady_clock::now();
+    double tm[6] = {0, 0, 0, 0, 0, 0};  // TV_VERBOSE=3: meminfo+reserve, sync, remap, create, map, access
+    auto lap = [&](int i, std::chrono::steady_clock::time_point& t) {
+        const auto n = std::chrono::steady_clock::now();
+        tm[i] += std::chrono::duration<double, std::milli>(n - t).count();
+        t = n;
+    };
+    auto tl = t0;
     const VmmApi& a = vmm();
     // geometric growth in >= 64 MB steps: few mappings per buffer
     size_t nb = std::max(bytes, 2 * b.bytes);
@@ -1139,26 +1158,64 @@ int ensure(Buf& b, size_t bytes, bool /*keep: contents are always kept*/ = false
         prop.location.id = t_build_device;
         size_t g = 0;
         if (a.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !g) g = 2u << 20;
-        nb = std::max(nb, static_cast<size_t>(64u << 20));
+        // TV_BUILD_VMM_TIGHT=1 (tests): granule-sized steps in exactly-sized ranges, so that every
+        // growth maps a new handle and moves the buffer to a new range
+        static const bool tight = std::getenv("TV_BUILD_VMM_TIGHT") && std::atoi(std::getenv("TV_BUILD_VMM_TIGHT"));
+        if (!tight) nb = std::max(nb, static_cast<size_t>(64u << 20));
         nb = (nb + g - 1) / g * g;
-        if (!b.va) {
+        if (nb > b.reserved) {
+            // Reserve a virtual range of 8x the request (>= 1 GB, <= device memory). Not the whole
+            // device per buffer: mapping into and freeing ~25 ranges of 178 GB each cost 0.1-3.4 s per
+            // build on B200 (tools/vmm_probe2.cu), against < 3 ms for ranges of a few GB. A buffer
+            // that outgrows its range moves: the same physical handles are mapped at a larger
+            // range (no copy) and the old range is released.
             size_t total = 0, free_b = 0;
             cudaMemGetInfo(&free_b, &total);
-            b.reserved = (std::max(total, nb) + g - 1) / g * g;  // virtual only
-            if (a.reserve(&b.va, b.reserved, g, 0, 0) != CUDA_SUCCESS)
+            size_t want = std::max(nb * 8, static_cast<size_t>(1) << 30);
+            want = tight ? nb : std::max(std::min(want, total), nb);
+            want = (want + g - 1) / g * g;
+            CUdeviceptr nva = 0;
+            if (a.reserve(&nva, want, g, 0, 0) != CUDA_SUCCESS)
                 return set_error(TV_ERR_OOM, "build alloc: cannot reserve a virtual range");
+            lap(0, tl);
+            if (b.bytes) {
+                cudaStreamSynchronize(0);  // kernels in flight may still use the old addresses
+                lap(1, tl);
+                CUmemAccessDesc d = {};
+                d.location = prop.location;
+                d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+                size_t off = 0;
+                bool ok = true;
+                for (size_t i = 0; i < b.handles.size() && ok; ++i) {
+                    ok = a.map(nva + off, b.sizes[i], 0, b.handles[i], 0) == CUDA_SUCCESS;
+                    off += b.sizes[i];
+                }
+                if (ok) ok = a.access(nva, b.bytes, &d, 1) == CUDA_SUCCESS;
+                if (!ok) {
+                    if (off) a.unmap(nva, off);
+                    a.addr_free(nva, want);
+                    return set_error(TV_ERR_OOM, "build alloc: remap failed");
+                }
+                a.unmap(b.va, b.bytes);
+                a.addr_free(b.va, b.reserved);
+                lap(2, tl);
+            }
+            b.va = nva;
+            b.reserved = want;
             b.p = reinterpret_cast<void*>(b.va);
             b.mapped = true;
         }
-        if (nb > b.reserved) return set_error(TV_ERR_OOM, "build alloc: buffer exceeds device memory");
         const size_t add = nb - b.bytes;
         CUmemGenericAllocationHandle h;
+        lap(5, tl);
         if (a.create(&h, add, &prop, 0) != CUDA_SUCCESS)
             return set_error(TV_ERR_OOM, "build alloc: out of device memory");
+        lap(3, tl);
         if (a.map(b.va + b.bytes, add, 0, h, 0) != CUDA_SUCCESS) {
             a.release(h);
             return set_error(TV_ERR_OOM, "build alloc: map failed");
         }
+        lap(4, tl);
         CUmemAccessDesc d = {};
         d.location = prop.location;
         d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
@@ -1167,8 +1224,16 @@ int ensure(Buf& b, size_t bytes, bool /*keep: contents are always kept*/ = false
             a.release(h);
             return set_error(TV_ERR_OOM, "build alloc: access failed");
         }
+        lap(5, tl);
+        if (poison()) cudaMemset(reinterpret_cast<char*>(b.va) + b.bytes, 0x5A, add);
         b.handles.push_back(h);
+        b.sizes.push_back(add);
         b.bytes = nb;
+        if (verbose3)
+            std::fprintf(stderr,
+                         "tetvol_b200: ensure %.1f -> %.1f MB: reserve %.2f sync %.2f remap %.2f create %.2f map %.2f "
+                         "access+rest %.2f ms\n",
+                         (nb - add) / 1048576.0, nb / 1048576.0, tm[0], tm[1], tm[2], tm[3], tm[4], tm[5]);
     } else {
         void* p = nullptr;
         cudaError_t e = cudaMalloc(&p, nb);
@@ -1180,6 +1245,7 @@ int ensure(Buf& b, size_t bytes, bool /*keep: contents are always kept*/ = false
                 return cuda_status(e, "build grow");
             }
         }
+        if (poison()) cudaMemset(static_cast<char*>(p) + b.bytes, 0x5A, nb - b.bytes);
         b.reset();
         b.p = p;
         b.bytes = nb;
@@ -1189,6 +1255,40 @@ int ensure(Buf& b, size_t bytes, bool /*keep: contents are always kept*/ = false
                      b.mapped ? "vmm" : "cudaMalloc",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     return TV_OK;
+}
+
+// The build's device scratch. Kept per device across builds (TV_BUILD_CACHE, default on) and
+// released by tv_build_trim: the buffers of a C4 build sum to ~45 GB, and re-creating them for
+// every build put 0.2-3 s of driver time (cuMemCreate / cudaMalloc of memory the previous build
+// just freed) into warm builds of 0.6 s. Every build initialises what it reads (TV_BUILD_POISON).
+struct BuildScratch {
+    std::mutex m;
+    Buf align[3];
+    Buf tets, tv4, verts, split, flags, stats, table, vtouch, owner, leaves, sel, tmp, mid, miss_hi, miss_lo,
+        miss_idx, miss_hi2, miss_lo2, miss_idx2, head, scan, misc, stripe, fresh, marked, khi, klo, rec, khi2, klo2,
+        rec2;
+    template <class F>
+    void each(F f) {
+        for (auto& b : align) f(b);
+        for (Buf* b : {&tets, &tv4, &verts, &split, &flags, &stats, &table, &vtouch, &owner, &leaves, &sel, &tmp,
+                       &mid, &miss_hi, &miss_lo, &miss_idx, &miss_hi2, &miss_lo2, &miss_idx2, &head, &scan, &misc,
+                       &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2})
+            f(*b);
+    }
+    void release() {
+        each([](Buf& b) { b.reset(); });
+    }
+    size_t bytes() {
+        size_t n = 0;
+        each([&](Buf& b) { n += b.bytes; });
+        return n;
+    }
+};
+
+std::mutex g_scratch_mu;
+std::map<int, BuildScratch*>& scratch_map() {
+    static auto* m = new std::map<int, BuildScratch*>();  // never destroyed: no CUDA calls at exit
+    return *m;
 }
 
 // host init_roots (tet_grid.cpp:184-233)
@@ -1251,7 +1351,7 @@ int host_camera(const tv_camera* c, CamView& v, d3 pn[5], double pd[5]);
 namespace {
 int build_grid_impl(const float* dens, const float* temp, const float* alb, int nx, int ny, int nz,
                     const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out,
-                    tv_build_stats* stats) {
+                    tv_build_stats* stats, BuildScratch& S) {
     int rc = validate_build_cfg(cfg);
     if (rc) return rc;
     if (cfg->use_camera && !camera) return set_error(TV_ERR_CONFIG, "useCamera set but no camera given");
@@ -1278,8 +1378,12 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     cudaEventRecord(e0);
 
     const uint64_t nvox = static_cast<uint64_t>(nx) * ny * nz;
-    Buf align_b[3];  // misaligned channels, copied (see below)
-    Buf tets_b, tv4_b, verts_b, split_b, flags_b, stats_b, table_b, vtouch_b, owner_b, leaves_b, sel_b, tmp_b, mid_b, miss_hi_b, miss_lo_b, miss_idx_b, miss_hi2_b, miss_lo2_b, miss_idx2_b, head_b, scan_b, misc_b;
+    Buf* align_b = S.align;  // misaligned channels, copied (see below)
+    Buf &tets_b = S.tets, &tv4_b = S.tv4, &verts_b = S.verts, &split_b = S.split, &flags_b = S.flags,
+        &stats_b = S.stats, &table_b = S.table, &vtouch_b = S.vtouch, &owner_b = S.owner, &leaves_b = S.leaves,
+        &sel_b = S.sel, &tmp_b = S.tmp, &mid_b = S.mid, &miss_hi_b = S.miss_hi, &miss_lo_b = S.miss_lo,
+        &miss_idx_b = S.miss_idx, &miss_hi2_b = S.miss_hi2, &miss_lo2_b = S.miss_lo2, &miss_idx2_b = S.miss_idx2,
+        &head_b = S.head, &scan_b = S.scan, &misc_b = S.misc;
     size_t cap_t = 0, cap_v = 0;
     uint64_t hmask = 0;
 
@@ -1411,8 +1515,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     uint32_t n_fresh = 24, n_marked = 0, n_leaves = 24;
     uint32_t fresh_lo = 0;                    // the fresh leaves' ids lie in [fresh_lo, n_t)
     constexpr uint32_t kStripeOwners = 32768;  // stripe up to 32K owners (64 MB of stripes)
-    Buf stripe_b;
-    Buf fresh_b, marked_b;
+    Buf &stripe_b = S.stripe, &fresh_b = S.fresh, &marked_b = S.marked;
     TRY(ensure(fresh_b, 24 * sizeof(uint32_t)));
     CK(cudaMemcpy(fresh_b.p, roots, sizeof(roots), cudaMemcpyHostToDevice), "fresh");
     int herr = 0;
@@ -1615,7 +1718,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     // ---- neighbour links by face pairing (tet_grid.cpp:130-152) ----
     {
         const uint64_t nf = 4ull * n_leaves;
-        Buf khi, klo, rec, khi2, klo2, rec2;
+        Buf &khi = S.khi, &klo = S.klo, &rec = S.rec, &khi2 = S.khi2, &klo2 = S.klo2, &rec2 = S.rec2;
         TRY(ensure(khi, nf * 8));
         TRY(ensure(klo, nf * 4));
         TRY(ensure(rec, nf * 4));
@@ -1719,7 +1822,52 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
 int build_grid(const float* dens, const float* temp, const float* alb, int nx, int ny, int nz,
                const tv_build_config* cfg, const tv_camera* camera, int device, tv_grid** out, tv_build_stats* stats) {
     t_build_device = device;
-    return build_grid_impl(dens, temp, alb, nx, ny, nz, cfg, camera, device, out, stats);
+    static const bool cache = !std::getenv("TV_BUILD_CACHE") || std::atoi(std::getenv("TV_BUILD_CACHE"));
+    if (!cache) {
+        BuildScratch local;
+        return build_grid_impl(dens, temp, alb, nx, ny, nz, cfg, camera, device, out, stats, local);
+    }
+    BuildScratch* S;
+    {
+        std::lock_guard<std::mutex> g(g_scratch_mu);
+        BuildScratch*& p = scratch_map()[device];
+        if (!p) p = new BuildScratch();
+        S = p;
+    }
+    std::lock_guard<std::mutex> lk(S->m);  // one build per device at a time
+    if (poison())
+        S->each([](Buf& b) {
+            if (b.bytes) cudaMemset(b.p, 0x5A, b.bytes);
+        });
+    const int rc = build_grid_impl(dens, temp, alb, nx, ny, nz, cfg, camera, device, out, stats, *S);
+    if (rc) S->release();  // a failed build (often out of memory) gives its scratch back
+    return rc;
+}
+
+int trim_scratch(int device) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::lock_guard<std::mutex> g(g_scratch_mu);
+    for (auto& kv : scratch_map()) {
+        if (device >= 0 && kv.first != device) continue;
+        std::lock_guard<std::mutex> lk(kv.second->m);
+        if (!kv.second->bytes()) continue;
+        cudaSetDevice(kv.first);
+        kv.second->release();
+    }
+    cudaSetDevice(cur);
+    return TV_OK;
+}
+
+size_t scratch_bytes(int device) {
+    std::lock_guard<std::mutex> g(g_scratch_mu);
+    size_t n = 0;
+    for (auto& kv : scratch_map())
+        if (device < 0 || kv.first == device) {
+            std::lock_guard<std::mutex> lk(kv.second->m);
+            n += kv.second->bytes();
+        }
+    return n;
 }
 
 }  // namespace tvb
@@ -1747,6 +1895,10 @@ int prevalidate(const tv_build_config* cfg, const tv_camera* camera) {
 extern "C" {
 
 int tv_check_build_config(const tv_build_config* cfg) { return validate_build_cfg(cfg); }
+
+int tv_build_trim(int device) { return trim_scratch(device); }
+
+uint64_t tv_build_scratch_bytes(int device) { return scratch_bytes(device); }
 
 int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, double value, float* out_dev,
                            int device) {

@@ -71,6 +71,8 @@ def test_no_cpu_fallback_without_gpu():
 
     if tv.device_count() > 0:
         pytest.skip("a GPU is present")
+    tv.build_trim()
+    assert tv.build_scratch_bytes() == 0
     vol = np.zeros((4, 4, 4), np.float32)
     with pytest.raises(tv.CudaError):
         tv.build_adaptive_grid(vol, tv.BuildConfig())

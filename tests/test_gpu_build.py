@@ -130,9 +130,9 @@ def test_build_config_errors(tv):
 
 
 def test_build_leaves_the_default_mempool_alone(tv):
-    """Build scratch lives in a private pool that is trimmed after the build
-    (ADVICE r01): the device's default pool keeps its release threshold, and
-    two builds of the same field give identical grids (determinism)."""
+    """Build scratch is the library's own (VMM mappings kept for the next
+    build): the device's default pool keeps its release threshold,
+    and two builds of the same field give identical grids (determinism)."""
     from cuda.bindings import runtime as rt
 
     err, pool = rt.cudaDeviceGetDefaultMemPool(0)
@@ -168,3 +168,53 @@ def test_build_from_misaligned_device_volume(tv):
     v2, t2, _ = g2.download()
     assert s1.leaf_count == s2.leaf_count
     assert np.array_equal(v1, v2) and np.array_equal(t1.view(np.uint8), t2.view(np.uint8))
+
+
+def test_build_scratch_allocators_agree(tv, tmp_path):
+    """Build scratch is VMM-backed and kept per device between builds
+    (tv_build_trim releases it). A buffer grows by mapping more physical memory
+    behind its pointer; one that outgrows its virtual range moves its handles
+    to a larger range without a copy. Each subprocess first builds a different
+    field (leaving stale scratch behind), then the cloud64 + camera grid:
+    default; TV_BUILD_VMM_TIGHT=1 (granule steps, exactly-sized ranges: every
+    growth is a move); TV_BUILD_NO_VMM=1 (cudaMalloc + copy); TV_BUILD_CACHE=0
+    (fresh scratch per build); TV_BUILD_POISON=1 (every byte a build has not
+    written reads 0x5A). All give the same grid."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import oracle as O, paper_2506_11510_b200 as tv; "
+            "tv.build_adaptive_grid(O.gen_volume('noise', 80), tv.BuildConfig(0.05, 14, False, 1.0, 3.0)); "
+            "held = tv.build_scratch_bytes(0); "
+            "cam = tv.PinholeCamera((0.5, 0.5, -1.2), (0, 0, 1), (0, 1, 0), 40, 1024, 1024); "
+            "g, s = tv.build_adaptive_grid(O.gen_volume('cloud', 64), tv.BuildConfig(0.15, 18, True, 1.0, 16.0), cam); "
+            "v, t, r = g.download(); np.savez(sys.argv[1], v=v, t=t.view(np.uint8), n=s.leaf_count, held=held)" % root)
+    out = {}
+    for name, env in [("vmm", {}), ("tight", {"TV_BUILD_VMM_TIGHT": "1"}), ("malloc", {"TV_BUILD_NO_VMM": "1"}),
+                      ("nocache", {"TV_BUILD_CACHE": "0"}), ("poison", {"TV_BUILD_POISON": "1"}),
+                      ("poison_tight", {"TV_BUILD_POISON": "1", "TV_BUILD_VMM_TIGHT": "1"})]:
+        f = str(tmp_path / f"{name}.npz")
+        e = dict(os.environ, **env)
+        subprocess.run([sys.executable, "-c", code, f], check=True, env=e, timeout=300)
+        out[name] = np.load(f)
+    assert int(out["vmm"]["n"]) == 361510
+    assert int(out["vmm"]["held"]) > 0 and int(out["nocache"]["held"]) == 0
+    for name in out:
+        assert np.array_equal(out[name]["v"], out["vmm"]["v"]), name
+        assert np.array_equal(out[name]["t"], out["vmm"]["t"]), name
+
+
+def test_build_trim_releases_scratch(tv):
+    vol = O.gen_volume("cloud", 40)
+    bc = tv.BuildConfig(0.3, 12, False, 1.0, 8.0)
+    g1, s1 = tv.build_adaptive_grid(vol, bc)
+    assert tv.build_scratch_bytes(0) > 0
+    tv.build_trim(0)
+    assert tv.build_scratch_bytes(0) == 0
+    g2, s2 = tv.build_adaptive_grid(vol, bc)
+    v1, t1, _ = g1.download()
+    v2, t2, _ = g2.download()
+    assert np.array_equal(v1, v2) and np.array_equal(t1.view(np.uint8), t2.view(np.uint8))
+    tv.build_trim()
