@@ -185,7 +185,19 @@ struct VolView {
     const float* temp;
     const float* alb;
     int nx, ny, nz;
+    // voxel centre coordinates per axis, (i + 0.5) / n (volume.hpp:44-46), and RN(1 / nx), RN(1 / ny)
+    // for the index -> (i, j, k) split (centres_kernel; voxel sweeps only)
+    const double *cx, *cy, *cz;
+    double rnx, rny;
 };
+
+// the same IEEE division the reference evaluates per voxel, once per coordinate
+__global__ void centres_kernel(int nx, int ny, int nz, double* c) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nx) c[t] = (t + 0.5) / nx;
+    else if (t < nx + ny) c[t] = (t - nx + 0.5) / ny;
+    else if (t < nx + ny + nz) c[t] = (t - nx - ny + 0.5) / nz;
+}
 
 struct CamCrit {
     d3 pos;
@@ -382,11 +394,29 @@ __device__ __forceinline__ uint32_t root_of(const RootScan& R, const uint4* vert
     return o;
 }
 
+// q = x / d for x < 2^37 (4096^3 voxels) through the f64 reciprocal: x * RN(1/d) is within
+// 2^-15 of x / d, so the truncated product is off by at most one and one correction each way
+// makes it exact (the integer divisions it replaces were 38 % of the sweep's instructions).
+__device__ __forceinline__ uint64_t div_small(uint64_t x, uint32_t d, double rd, uint32_t& rem) {
+    uint64_t q = static_cast<uint64_t>(static_cast<double>(x) * rd);
+    int64_t r = static_cast<int64_t>(x - q * d);
+    if (r < 0) --q, r += d;
+    else if (r >= static_cast<int64_t>(d)) ++q, r -= d;
+    rem = static_cast<uint32_t>(r);
+    return q;
+}
+
+__device__ __forceinline__ void voxel_ijk(const VolView& V, uint64_t idx, int& i, int& j, int& k) {
+    uint32_t ri, rj;
+    const uint64_t row = div_small(idx, V.nx, V.rnx, ri);
+    k = static_cast<int>(div_small(row, V.ny, V.rny, rj));
+    i = static_cast<int>(ri), j = static_cast<int>(rj);
+}
+
 __device__ __forceinline__ d3 voxel_centre(const VolView& V, uint64_t idx) {
-    const uint64_t row = idx / V.nx;
-    const int i = static_cast<int>(idx - row * V.nx), j = static_cast<int>(row % V.ny),
-              k = static_cast<int>(row / V.ny);
-    return mk((i + 0.5) / V.nx, (j + 0.5) / V.ny, (k + 0.5) / V.nz);  // volume.hpp:44-46
+    int i, j, k;
+    voxel_ijk(V, idx, i, j, k);
+    return mk(__ldg(V.cx + i), __ldg(V.cy + j), __ldg(V.cz + k));  // (i + 0.5) / nx ... (volume.hpp:44-46)
 }
 
 // descent from a bisected owner to the leaf holding p (tet_grid.cpp:453-470)
@@ -513,22 +543,29 @@ __global__ void __launch_bounds__(kVoxThreads, mode == kVoxDescend ? 4 : 3) vox_
             const uint32_t dq = (dirty >> (4 * q)) & 15u;
             if (g >= n4 || !dq) continue;
             const uint64_t idx0 = 4 * g;
+            // the group's centres: one index split when the group lies in one x row (nx % 4 == 0)
+            int gi = 0, gj = 0, gk = 0;
+            if (mode != kVoxAll && (V.nx & 3) == 0) voxel_ijk(V, idx0, gi, gj, gk);
+            auto centre = [&](int t) -> d3 {
+                if ((V.nx & 3) == 0) return mk(__ldg(V.cx + gi + t), __ldg(V.cy + gj), __ldg(V.cz + gk));
+                return voxel_centre(V, idx0 + t);
+            };
             uint4 o4;
             if (mode == kVoxInit) {
-                o4.x = root_of(R, verts, voxel_centre(V, idx0));
-                o4.y = root_of(R, verts, voxel_centre(V, idx0 + 1));
-                o4.z = root_of(R, verts, voxel_centre(V, idx0 + 2));
-                o4.w = root_of(R, verts, voxel_centre(V, idx0 + 3));
+                o4.x = root_of(R, verts, centre(0));
+                o4.y = root_of(R, verts, centre(1));
+                o4.z = root_of(R, verts, centre(2));
+                o4.w = root_of(R, verts, centre(3));
                 own4[g] = o4;
             } else {
                 o4 = own4[g];
             }
             const float4 d4 = d4p[g];
             if (mode == kVoxDescend) {  // dense chunk: descend the dirty voxels of the group
-                if (dq & 1u) o4.x = descend(split, flags, o4.x, voxel_centre(V, idx0));
-                if (dq & 2u) o4.y = descend(split, flags, o4.y, voxel_centre(V, idx0 + 1));
-                if (dq & 4u) o4.z = descend(split, flags, o4.z, voxel_centre(V, idx0 + 2));
-                if (dq & 8u) o4.w = descend(split, flags, o4.w, voxel_centre(V, idx0 + 3));
+                if (dq & 1u) o4.x = descend(split, flags, o4.x, centre(0));
+                if (dq & 2u) o4.y = descend(split, flags, o4.y, centre(1));
+                if (dq & 4u) o4.z = descend(split, flags, o4.z, centre(2));
+                if (dq & 8u) o4.w = descend(split, flags, o4.w, centre(3));
                 own4[g] = o4;
             }
             if (dq & 1u) vox_add(st, L, o4.x, d4.x, V, idx0, with_tl);
@@ -1266,13 +1303,13 @@ struct BuildScratch {
     Buf align[3];
     Buf tets, tv4, verts, split, flags, stats, table, vtouch, owner, leaves, sel, tmp, mid, miss_hi, miss_lo,
         miss_idx, miss_hi2, miss_lo2, miss_idx2, head, scan, misc, stripe, fresh, marked, khi, klo, rec, khi2, klo2,
-        rec2;
+        rec2, centres;
     template <class F>
     void each(F f) {
         for (auto& b : align) f(b);
         for (Buf* b : {&tets, &tv4, &verts, &split, &flags, &stats, &table, &vtouch, &owner, &leaves, &sel, &tmp,
                        &mid, &miss_hi, &miss_lo, &miss_idx, &miss_hi2, &miss_lo2, &miss_idx2, &head, &scan, &misc,
-                       &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2})
+                       &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2, &centres})
             f(*b);
     }
     void release() {
@@ -1407,7 +1444,11 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             CK(cudaMemcpy(align_b[c].p, ch[c], nvox * sizeof(float), cudaMemcpyDeviceToDevice), "align volume");
             ch[c] = align_b[c].as<float>();
         }
-    const VolView V{ch[0], ch[1], ch[2], nx, ny, nz};
+    TRY(ensure(S.centres, static_cast<size_t>(nx + ny + nz) * sizeof(double)));
+    double* cxyz = S.centres.as<double>();
+    centres_kernel<<<nblk(nx + ny + nz, 256), 256>>>(nx, ny, nz, cxyz);
+    CK(cudaGetLastError(), "voxel centres");
+    const VolView V{ch[0], ch[1], ch[2], nx, ny, nz, cxyz, cxyz + nx, cxyz + nx + ny, 1.0 / nx, 1.0 / ny};
 
     auto grow_tets = [&](size_t need) -> int {
         if (need <= cap_t) return TV_OK;

@@ -23,9 +23,9 @@ def field(n):
 
 
 def build(vol, n, thr, ml, camera=True):
-    """two builds: the first pays the memory pool's growth (fresh device memory
-    is mapped and scrubbed at about 10 GB/s), the second reuses it; returns the
-    second grid, its stats, and the first build's device seconds"""
+    """two builds: the first of a size grows the build scratch (VMM mappings,
+    kept per device between builds), the second reuses it; returns the second
+    grid, its stats, and the first build's device seconds"""
     cam = tv.PinholeCamera(**CAM) if camera else None
     g, st = tv.build_adaptive_grid_dev(vol.data_ptr(), (n, n, n), tv.BuildConfig(thr, ml, camera, 1.0, 16.0), cam)
     torch.cuda.synchronize()
