@@ -874,9 +874,6 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
     split[t] = r;
 }
 
-#ifndef TV_HANG_EAGER
-#define TV_HANG_EAGER 0
-#endif
 // Mark every leaf with a hanging edge (an edge whose integer midpoint is a
 // vertex), over all tet ids. Only two kinds of leaf can have one: the children
 // made by the last bisect pass (ids >= first_new) and older leaves with at
@@ -887,15 +884,9 @@ __global__ void hanging_kernel(uint32_t n_t, uint32_t first_new, const uint4* __
                                const uint32_t* __restrict__ vtouch, uint8_t* flags) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_t) return;
-#if TV_HANG_EAGER
-    const uint4 tv = tv4[t];  // issued with the flags load: one dependent level less, twice the tv4 bytes
-    const uint8_t f = flags[t];
-    if (!(f & F_LEAF)) return;
-#else
     const uint8_t f = flags[t];
     if (!(f & F_LEAF)) return;
     const uint4 tv = tv4[t];
-#endif
     if (t < first_new) {
         auto bit = [&](uint32_t v) { return (__ldg(vtouch + (v >> 5)) >> (v & 31)) & 1u; };
         if (bit(tv.x) + bit(tv.y) + bit(tv.z) + bit(tv.w) < 2) return;
