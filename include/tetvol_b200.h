@@ -11,6 +11,7 @@
  *   tv_build            <- build_adaptive_grid(vol, cfg, camera, stats)
  *                          (builder.hpp:51-52)
  *   tv_render           <- render(grid, camera, cfg, threads) (tracer.hpp:84-85)
+ *   tv_render_multi     <- render() over several GPUs from one process
  *   tv_render_tiles     <- the per-rank share of render() for multi-GPU
  *                          image-space sharding (interleaved 16x16 tiles)
  *   tv_march_segments   <- march_segments(grid, ray, stats) (tracer.hpp:49)
@@ -233,6 +234,16 @@ int tv_generate_volume_dev(int32_t kind, int32_t nx, int32_t ny, int32_t nz, dou
 /* -- render ------------------------------------------------------------------ */
 int tv_render(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg, tv_framebuffer* out,
               tv_render_stats* stats);
+/* render() over several GPUs from one process: grids[r]
+ * (normally the same grid, uploaded or built once per device) renders the
+ * interleaved 16x16 tiles t with t % n == r on its device, one host thread per
+ * rank. Ranks whose device has peer access to grids[0]'s device store their
+ * pixels straight into the frame there (NVLink); others render a private frame
+ * whose tiles are merged on the host. The framebuffer is bit-identical to
+ * tv_render's for any n; stats->seconds is the slowest rank's device time.
+ * Synchronous; one tv_render_multi call runs at a time. */
+int tv_render_multi(const tv_grid* const* grids, int32_t n, const tv_camera* camera, const tv_render_config* cfg,
+                    tv_framebuffer* out, tv_render_stats* stats);
 /* Multi-GPU share: renders the interleaved 16x16 tiles t with
  * t % n_ranks == rank (tile t = row-major over ceil(W/16) x ceil(H/16)).
  * Outputs are DEVICE pointers to full-frame buffers (only this rank's pixels

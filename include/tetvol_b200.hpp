@@ -154,6 +154,25 @@ inline ImageAccumulator render(const DeviceGrid& grid, const PinholeCamera& came
     return acc;
 }
 
+// render() over several GPUs from one process: one DeviceGrid per device
+// (the same grid uploaded or built on each); the same ImageAccumulator bit for bit.
+inline ImageAccumulator render_multi(const std::vector<const DeviceGrid*>& grids, const PinholeCamera& camera,
+                                     const RenderConfig& cfg) {
+    ImageAccumulator acc(camera.width(), camera.height());
+    tv_framebuffer fb{acc.sum.data(), acc.sum_sq.data(), acc.sample_counts.data()};
+    tv_render_stats st{};
+    const tv_camera c = to_c(camera);
+    const tv_render_config r = to_c(cfg);
+    std::vector<const tv_grid*> hs;
+    for (const DeviceGrid* g : grids) hs.push_back(g->handle());
+    check(tv_render_multi(hs.data(), static_cast<int32_t>(hs.size()), &c, &r, &fb, &st));
+    acc.cells_visited = st.cells_visited;
+    acc.paths_traced = st.paths_traced;
+    acc.degenerate_paths = st.degenerate_paths;
+    acc.seconds = st.seconds;
+    return acc;
+}
+
 // Drop-in overload on a host TetGrid (uploads once per call).
 inline ImageAccumulator render(const TetGrid& grid, const PinholeCamera& camera, const RenderConfig& cfg,
                                int threads = 0, int device = 0) {

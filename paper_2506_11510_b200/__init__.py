@@ -161,6 +161,8 @@ _sig("tv_build_dev", C.c_int, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POI
 _sig("tv_build_trim", C.c_int, C.c_int)
 _sig("tv_build_scratch_bytes", C.c_uint64, C.c_int)
 _sig("tv_generate_volume_dev", C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, C.c_int)
+_sig("tv_render_multi", C.c_int, C.POINTER(_P), C.c_int32, C.POINTER(_Camera), C.POINTER(_RenderConfig),
+     C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
 _sig("tv_render", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.POINTER(_Framebuffer),
      C.POINTER(_RenderStats))
 _sig("tv_render_tiles", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.c_int32, C.c_int32, _P, _P, _P,
@@ -408,6 +410,24 @@ def render(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, threads: int
     st = _RenderStats()
     cam, rc = camera._c(), cfg._c()
     _check(_lib.tv_render(grid.handle, C.byref(cam), C.byref(rc), C.byref(fb), C.byref(st)))
+    return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
+
+
+def render_multi(grids, camera: PinholeCamera, cfg: RenderConfig) -> ImageAccumulator:
+    """render() over several GPUs from one process: grids[r] (one per device,
+    normally the same grid uploaded or built on each) renders the interleaved
+    16x16 tiles t % len(grids) == r; the result equals render()'s bit for bit.
+    ``seconds`` is the slowest rank's device time."""
+    grids = list(grids)
+    w, h = int(camera.width), int(camera.height)
+    s = np.zeros(w * h * 3)
+    sq = np.zeros(w * h * 3)
+    cnt = np.zeros(w * h, np.uint32)
+    fb = _Framebuffer(s.ctypes.data_as(_D), sq.ctypes.data_as(_D), cnt.ctypes.data_as(_U32))
+    st = _RenderStats()
+    cam, rc = camera._c(), cfg._c()
+    hs = (_P * len(grids))(*[g.handle for g in grids])
+    _check(_lib.tv_render_multi(hs, len(grids), C.byref(cam), C.byref(rc), C.byref(fb), C.byref(st)))
     return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
 
 
@@ -664,6 +684,6 @@ __all__ = [
     "ImageAccumulator", "IoError", "load_grid", "save_grid", "spot_rays",
     "OutsideGrid", "PinholeCamera", "RenderConfig", "TET_DTYPE", "SEGMENT_DTYPE", "TetGrid", "TetvolError",
     "build_adaptive_grid", "build_adaptive_grid_dev", "build_scratch_bytes", "build_trim", "device_count", "generate_volume_dev", "locate_points",
-    "march_segments", "march_transmittance", "trace", "sample_free_path", "FREE_PATH_DTYPE", "render", "render_into", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",
+    "march_segments", "march_transmittance", "trace", "sample_free_path", "FREE_PATH_DTYPE", "render", "render_into", "render_multi", "render_reference", "render_tiles", "tile_pack", "tile_pack_words",
     "tile_unpack", "version",
 ]

@@ -3,12 +3,14 @@
 // the pinhole camera precompute, device memory management and kernel launches.
 // No exception crosses this boundary.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <memory>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tv_trace.cuh"
@@ -176,10 +178,16 @@ struct Workspace {
         uint32_t* cost = nullptr;   // TV_TILE_ORDER=3: tet steps per list position in the last frame
     };
     std::map<TileOrderKey, TileTables> tile_orders;
+    // tv_render_multi (one call at a time, g_multi_mu): the frame's accumulators
+    // when this is the first grid's device, else this rank's stats words (and
+    // its private frame when it cannot reach the first device)
+    void* multi = nullptr;
+    size_t multi_bytes = 0;
     int tile_mode = 1;
     double tile_radius = 0.8;  // outer tiles: beyond this fraction of the inscribed circle
 };
 Workspace g_ws[64];
+std::mutex g_multi_mu;
 constexpr uint32_t kSortTiles = 4096;  // TV_TILE_ORDER=3 sorts at most this many tiles per rank
 
 int env_int(const char* name, int dflt) {
@@ -641,6 +649,158 @@ int tv_render_accumulate(const tv_grid* h, const tv_camera* camera, const tv_ren
     RenderOut ro{sum_dev, sum_sq_dev, counts_dev, stats_dev, peer_outputs(g.device, sum_dev, sum_sq_dev, counts_dev)};
     return render_frame(g, cv, make_params(cfg), rank, n_ranks, ro, *w, static_cast<cudaStream_t>(stream),
                         static_cast<uint32_t>(first_sample));
+}
+
+// One process, several GPUs (SURVEY.md 8(b) tv_render_multi): rank r renders
+// the interleaved 16x16 tiles t with t % n == r on grids[r]'s device, one host
+// thread per rank. Where the device can reach the first grid's device directly
+// (P2P over NVLink), the rank's accumulate kernel stores its pixels straight
+// into the frame on that device (the gather fused into the render, as
+// tv_render_tiles with peer outputs); otherwise the rank renders a private
+// full frame and its tiles are merged on the host. Every pixel is rendered by
+// one rank with the reference's per-pixel sample order, so the framebuffer is
+// bit-identical to tv_render's for any n (two ranks on one device serialise on
+// its stream and stay correct).
+int tv_render_multi(const tv_grid* const* grids, int32_t n, const tv_camera* camera, const tv_render_config* cfg,
+                    tv_framebuffer* out, tv_render_stats* stats) {
+    if (!grids || n < 1) return set_error(TV_ERR_ARG, "need at least one grid");
+    for (int r = 0; r < n; ++r)
+        if (!grids[r]) return set_error(TV_ERR_ARG, "grid is null");
+    int rc = validate_render(cfg);
+    if (rc) return rc;
+    CamView cv;
+    if ((rc = host_camera(camera, cv, nullptr, nullptr))) return rc;
+    const int dev0 = grids[0]->g.device;
+    const uint64_t npx = static_cast<uint64_t>(cv.w) * cv.h;
+    const size_t frame_bytes = npx * (6 * sizeof(double) + sizeof(uint32_t));
+    const size_t stats_off = (frame_bytes + 255) & ~static_cast<size_t>(255);
+    const size_t bytes = stats_off + 32 * static_cast<size_t>(n);  // + 4 stats words per rank
+    const RenderParams rp = make_params(cfg);
+    const uint32_t tiles_x = (static_cast<uint32_t>(cv.w) + 15) / 16, tiles_y = (static_cast<uint32_t>(cv.h) + 15) / 16;
+
+    if ((rc = use_device(dev0))) return rc;
+    Workspace* w0;
+    if ((rc = workspace(dev0, w0))) return rc;
+    std::lock_guard<std::mutex> lk0(g_multi_mu);  // one multi-GPU frame at a time (the multi buffers)
+    if ((rc = grow(w0->multi, w0->multi_bytes, bytes, w0->idle))) return rc;
+    char* f0 = static_cast<char*>(w0->multi);
+    // which ranks write into dev0's frame: dev0 itself, and devices with peer access to it
+    std::vector<int> direct(n, 1);
+    const bool peer_ok = env_int("TV_MULTI_PEER", 1) != 0;  // 0 (tests): every rank > 0 takes the host merge
+    for (int r = 0; r < n; ++r) {
+        const int d = grids[r]->g.device;
+        if (r > 0 && !peer_ok) {
+            direct[r] = 0;
+            continue;
+        }
+        if (d == dev0) continue;
+        int ok = 0;
+        if (cudaDeviceCanAccessPeer(&ok, d, dev0) != cudaSuccess || !ok) {
+            cudaGetLastError();
+            direct[r] = 0;
+            continue;
+        }
+        if ((rc = use_device(d))) return rc;
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dev0, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return cuda_status(e, "peer access");
+    }
+    std::vector<int> rcs(n, TV_OK);
+    std::vector<std::string> msgs(n);
+    std::vector<std::array<uint64_t, 3>> hst(n, std::array<uint64_t, 3>{0, 0, 0});
+    std::vector<std::vector<char>> priv(n);  // host copies of the private frames
+    std::vector<double> ms(n, 0.0);
+    auto rank_fn = [&](int r) {
+        auto fail = [&](int code) {
+            rcs[r] = code;
+            msgs[r] = g_err;
+        };
+        const DeviceGrid& g = grids[r]->g;
+        int c = use_device(g.device);
+        if (c) return fail(c);
+        Workspace* w;
+        if ((c = workspace(g.device, w))) return fail(c);
+        std::lock_guard<std::mutex> lk(w->mu);  // ranks sharing a device run one after the other
+        // this rank's stats words: in the frame's block on dev0, else in its own device's
+        uint64_t* st = reinterpret_cast<uint64_t*>(f0 + stats_off) + 4 * r;
+        if (g.device != dev0) {
+            if ((c = grow(w->multi, w->multi_bytes, 256, w->idle))) return fail(c);
+            st = static_cast<uint64_t*>(w->multi);
+        }
+        // a rank that cannot write dev0's frame renders a private one (merged on the host)
+        char* frame = f0;
+        struct Priv {
+            void* p = nullptr;
+            ~Priv() { cudaFree(p); }
+        } pv;
+        if (!direct[r]) {
+            const cudaError_t e = cudaMalloc(&pv.p, frame_bytes);
+            if (e != cudaSuccess) return fail(cuda_status(e, "private frame"));
+            frame = static_cast<char*>(pv.p);
+        }
+        double* sum = reinterpret_cast<double*>(frame);
+        RenderOut ro{sum, sum + 3 * npx, reinterpret_cast<uint32_t*>(sum + 6 * npx), st,
+                     g.device != dev0 && direct[r] ? 1 : 0};
+        cudaStream_t sm = w->stream;
+        cudaError_t e = cudaMemsetAsync(st, 0, 3 * sizeof(uint64_t), sm);
+        if (e == cudaSuccess) e = cudaEventRecord(w->ev0, sm);
+        if (e != cudaSuccess) return fail(cuda_status(e, "multi frame start"));
+        if ((c = render_frame(g, cv, rp, r, n, ro, *w, sm))) return fail(c);
+        e = cudaEventRecord(w->ev1, sm);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hst[r].data(), st, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, sm);
+        if (e == cudaSuccess && !direct[r]) {
+            priv[r].resize(frame_bytes);
+            e = cudaMemcpyAsync(priv[r].data(), frame, frame_bytes, cudaMemcpyDeviceToHost, sm);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(sm);
+        if (e != cudaSuccess) return fail(cuda_status(e, "multi frame"));
+        float t = 0.f;
+        cudaEventElapsedTime(&t, w->ev0, w->ev1);
+        ms[r] = t;
+    };
+    {
+        std::vector<std::thread> th;
+        for (int r = 1; r < n; ++r) th.emplace_back(rank_fn, r);
+        rank_fn(0);
+        for (auto& t : th) t.join();
+    }
+    for (int r = 0; r < n; ++r)
+        if (rcs[r]) return set_error(rcs[r], "rank " + std::to_string(r) + ": " + msgs[r]);
+    if ((rc = use_device(dev0))) return rc;
+    double* sum = reinterpret_cast<double*>(f0);
+    if (out && out->sum) TV_CK(cudaMemcpy(out->sum, sum, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    if (out && out->sum_sq)
+        TV_CK(cudaMemcpy(out->sum_sq, sum + 3 * npx, 3 * npx * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    if (out && out->sample_counts)
+        TV_CK(cudaMemcpy(out->sample_counts, sum + 6 * npx, npx * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H");
+    // ranks without peer access: their tiles from their private frames
+    for (int r = 0; r < n && out; ++r) {
+        if (direct[r]) continue;
+        const double* ps = reinterpret_cast<const double*>(priv[r].data());
+        const uint32_t* pc = reinterpret_cast<const uint32_t*>(ps + 6 * npx);
+        for (uint32_t t = static_cast<uint32_t>(r); t < tiles_x * tiles_y; t += static_cast<uint32_t>(n)) {
+            const uint32_t x0 = (t % tiles_x) * 16, y0 = (t / tiles_x) * 16;
+            const uint32_t x1 = std::min<uint32_t>(x0 + 16, cv.w), y1 = std::min<uint32_t>(y0 + 16, cv.h);
+            for (uint32_t y = y0; y < y1; ++y) {
+                const uint64_t p = static_cast<uint64_t>(y) * cv.w + x0, m = x1 - x0;
+                if (out->sum) std::memcpy(out->sum + 3 * p, ps + 3 * p, 3 * m * sizeof(double));
+                if (out->sum_sq) std::memcpy(out->sum_sq + 3 * p, ps + 3 * npx + 3 * p, 3 * m * sizeof(double));
+                if (out->sample_counts) std::memcpy(out->sample_counts + p, pc + p, m * sizeof(uint32_t));
+            }
+        }
+    }
+    if (stats) {
+        stats->cells_visited = stats->degenerate_paths = 0;
+        double worst = 0.0;
+        for (int r = 0; r < n; ++r) {
+            stats->cells_visited += hst[r][0];
+            stats->degenerate_paths += hst[r][2];
+            worst = std::max(worst, ms[r]);
+        }
+        stats->paths_traced = npx * static_cast<uint64_t>(cfg->spp);
+        stats->seconds = worst * 1e-3;  // the slowest rank's device time
+    }
+    return TV_OK;
 }
 
 int tv_check_camera(const tv_camera* camera) {

@@ -97,6 +97,14 @@ int main() {
     REQUIRE(std::memcmp(a.sum_sq.data(), b.sum_sq.data(), a.sum_sq.size() * sizeof(double)) == 0);
     REQUIRE(a.sample_counts == b.sample_counts);
 
+    // render_multi(): three ranks (all on device 0 here) give the same accumulator
+    b200::DeviceGrid dg2(ref);
+    ImageAccumulator m = b200::render_multi({&dg, &dg2, &dg}, cam, rc);
+    REQUIRE(m.cells_visited == a.cells_visited);
+    REQUIRE(std::memcmp(a.sum.data(), m.sum.data(), a.sum.size() * sizeof(double)) == 0);
+    REQUIRE(std::memcmp(a.sum_sq.data(), m.sum_sq.data(), a.sum_sq.size() * sizeof(double)) == 0);
+    REQUIRE(a.sample_counts == m.sample_counts);
+
     // build_adaptive_grid(): GPU build, downloaded, passes validate(), same leaves
     BuildStats st;
     b200::DeviceGrid built = b200::build_adaptive_grid(vol, bc, nullptr, &st);

@@ -173,3 +173,36 @@ def test_peer_frame_direct_writes_two_processes():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+@pytest.mark.parametrize("peer", ["1", "0"])
+def test_render_multi_one_process_bit_identical(peer, monkeypatch):
+    """tv_render_multi: one process, one host thread per rank.
+    On this one-GPU box every rank's grid lives on device 0 (ranks sharing a
+    device run one after another); TV_MULTI_PEER=0 sends every rank > 0
+    through the private-frame + host-merge path that devices without peer
+    access take. Each way the frame equals tv_render's bit for bit."""
+    import paper_2506_11510_b200 as tv
+
+    monkeypatch.setenv("TV_MULTI_PEER", peer)
+    g = O.fuzzed(O.c_oracle(), 250, 0x93)
+    p = g.pools()
+    rng = np.random.default_rng(5)
+    lm = p.leaf_mask
+    p.tets["density"][lm] = rng.random(lm.sum()).astype(np.float32) * 5
+    p.tets["mask"][lm] = 1
+    dg = tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots, p.max_level)
+    dg2 = tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots, p.max_level)
+    W, H = 90, 75  # ragged last tile row / column
+    cam = tv.PinholeCamera((0.5, 0.5, -1.4), (0, 0, 1), (0, 1, 0), 50, W, H)
+    rc = tv.RenderConfig(spp=3, max_bounces=12, seed=6)
+    full = tv.render(dg, cam, rc)
+    for grids in ([dg], [dg, dg2], [dg, dg2, dg], [dg2] * 5):
+        m = tv.render_multi(grids, cam, rc)
+        assert np.array_equal(m.sum.view(np.uint64), full.sum.view(np.uint64)), len(grids)
+        assert np.array_equal(m.sum_sq.view(np.uint64), full.sum_sq.view(np.uint64)), len(grids)
+        assert np.array_equal(m.sample_counts, full.sample_counts), len(grids)
+        assert m.cells_visited == full.cells_visited and m.paths_traced == full.paths_traced
+        assert m.degenerate_paths == full.degenerate_paths
+    with pytest.raises(ValueError, match="at least one grid"):
+        tv.render_multi([], cam, rc)
