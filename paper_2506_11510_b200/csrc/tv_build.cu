@@ -257,6 +257,9 @@ __global__ void stats_zero_kernel(const uint32_t* list, uint32_t n, Stats* st, u
 // them is certified against a rounding bound (err_bound) or replayed
 // sequentially in voxel-index order.
 enum : int { kVoxInit = 0, kVoxDescend = 1, kVoxAll = 2 };
+#ifndef TV_VOX_DESC_BLOCKS
+#define TV_VOX_DESC_BLOCKS 4  // blocks of kVoxThreads per SM in the descend rounds (register cap)
+#endif
 constexpr int kVoxThreads = 256;
 
 struct Agg {
@@ -467,9 +470,13 @@ __device__ __forceinline__ void vox_add(const StatsSink& st, VoxLane& L, uint32_
 }
 
 template <int mode>
-__global__ void __launch_bounds__(kVoxThreads, mode == kVoxDescend ? 4 : 3) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
+__global__ void __launch_bounds__(kVoxThreads, mode == kVoxDescend ? TV_VOX_DESC_BLOCKS : 3) vox_stats_kernel(VolView V, RootScan R, const uint4* verts,
                                                                  const NodeRec* split, const uint8_t* flags,
-                                                                 uint32_t* owner, StatsSink st, int with_tl) {
+                                                                 uint32_t* owner, StatsSink st, int with_tl_arg) {
+    // the temperature / albedo sums exist in the payload pass only: a compile-time
+    // flag lets the other modes drop their registers and instructions
+    constexpr bool with_tl = mode == kVoxAll;
+    (void)with_tl_arg;
     const uint64_t nvox = static_cast<uint64_t>(V.nx) * V.ny * V.nz;
     const uint64_t n4 = nvox / 4;
     const int lane = threadIdx.x & 31;
