@@ -189,6 +189,9 @@ struct VolView {
     // for the index -> (i, j, k) split (centres_kernel; voxel sweeps only)
     const double *cx, *cy, *cz;
     double rnx, rny;
+    // brick owners (see "voxel bricks"); null: the owner map alone is authoritative
+    const uint32_t* brick;
+    int gbx, gby;
 };
 
 // the same IEEE division the reference evaluates per voxel, once per coordinate
@@ -601,6 +604,250 @@ __global__ void __launch_bounds__(kVoxThreads, mode == kVoxDescend ? TV_VOX_DESC
     }
 }
 
+// ------------------------------------------------------------ voxel bricks
+// While the leaves are much larger than a voxel (the early rounds), nearly
+// every voxel of a bisected leaf goes to the same child as its neighbours. The
+// volume is therefore also tiled into 8x8x8 bricks. A brick whose 512 voxels
+// all have one owner keeps that owner in brick_owner[b] (its per-voxel owner
+// words are not maintained) plus its precomputed density statistics. When its
+// owner is bisected, the brick descends as a whole while the split plane keeps
+// its eight corner centres strictly on one side (margin 1e-9 |n|_1; the side
+// test of every voxel centre inside is then the same, FP rounding included),
+// and its statistics go to the child leaf in one add. A brick that a plane
+// cuts becomes mixed: it joins the mixed list, and from then on its voxels
+// are handled one by one (brick_voxels_kernel). Bricks cut by the volume
+// border are mixed from the start. The owner of voxel v is brick_owner[b(v)]
+// unless that is kBrickMixed, then owner[v] (owner_at).
+constexpr int kBrick = 8;  // brick edge in voxels (4 was measured: more brick overhead than it saves)
+constexpr int kBrickLog = 3;
+constexpr int kBrickVox = kBrick * kBrick * kBrick;
+constexpr uint32_t kBrickMixed = 0xffffffffu;  // mixed: per-voxel owner words valid
+constexpr uint32_t kBrickFresh = 0x80000000u;  // | o: mixed this round; every voxel's owner is still o
+struct BrickStat {
+    double sum, asum;
+    uint32_t cnt, mn, mx, pad;
+};
+
+__device__ __forceinline__ uint32_t owner_at(const VolView& V, const uint32_t* owner, int i, int j, int k,
+                                             uint64_t idx) {
+    if (V.brick) {
+        const uint32_t bo =
+            V.brick[(static_cast<uint64_t>(k >> kBrickLog) * V.gby + (j >> kBrickLog)) * V.gbx + (i >> kBrickLog)];
+        if (bo != kBrickMixed) return bo;
+    }
+    return owner[idx];
+}
+
+__device__ __forceinline__ void list_append(uint32_t* list, uint32_t* n, uint32_t b, bool add) {
+    const unsigned m = __ballot_sync(0xffffffffu, add);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == lead) base = atomicAdd(n, static_cast<uint32_t>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, lead);
+    if (add) list[base + __popc(m & ((1u << lane) - 1u))] = b;
+}
+
+// after round 0's root scan: one warp per brick; a full brick whose voxels share
+// one owner becomes uniform (with its statistics), every other brick mixed
+__global__ void brick_init_kernel(VolView V, const uint32_t* owner, uint32_t* brick, BrickStat* bstat,
+                                  uint32_t* mixed, uint32_t* n_mixed) {
+    const uint32_t n_b = static_cast<uint32_t>(V.gbx) * V.gby * ((V.nz + kBrick - 1) / kBrick);
+    const int lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t b = w0; b < n_b; b += nw) {  // warp-uniform loop
+        const int bx = static_cast<int>(b % V.gbx), by = static_cast<int>((b / V.gbx) % V.gby),
+                  bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
+        const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
+        const bool full = x0 + kBrick <= V.nx && y0 + kBrick <= V.ny && z0 + kBrick <= V.nz;
+        uint32_t o0 = kBrickMixed;
+        bool same = full;
+        double sum = 0.0, asum = 0.0;
+        uint32_t mn = 0xffffffffu, mx = 0u;
+        if (full) {
+            o0 = owner[(static_cast<uint64_t>(z0) * V.ny + y0) * V.nx + x0];
+            for (int v = lane; v < kBrickVox; v += 32) {  // x fastest: lanes read consecutive voxels
+                const int x = x0 + (v & (kBrick - 1)), y = y0 + ((v >> kBrickLog) & (kBrick - 1)),
+                          z = z0 + (v >> (2 * kBrickLog));
+                const uint64_t idx = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x;
+                same &= owner[idx] == o0;
+                const float d = V.dens[idx];
+                sum += static_cast<double>(d);
+                asum += fabs(static_cast<double>(d));
+                mn = min(mn, ord_f(d));
+                mx = max(mx, ord_f(d));
+            }
+            same = __all_sync(0xffffffffu, same);
+        }
+        if (same) {
+            sum = wsum(sum);
+            asum = wsum(asum);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            if (lane == 0) {
+                brick[b] = o0;
+                bstat[b] = BrickStat{sum, asum, static_cast<uint32_t>(kBrickVox), mn, mx, 0u};
+            }
+        } else if (lane == 0) {
+            brick[b] = kBrickMixed;
+            const uint32_t at = atomicAdd(n_mixed, 1u);
+            mixed[at] = b;
+        }
+    }
+}
+
+// K1 of a round: every uniform brick whose owner was bisected descends as a
+// whole while its corners agree, or becomes mixed (fresh) at the first plane
+// that cuts it. One thread per brick.
+__global__ void brick_descend_kernel(VolView V, uint32_t n_b, uint32_t* brick, const BrickStat* bstat,
+                                     const NodeRec* split, const uint8_t* flags, StatsSink st, uint32_t* mixed,
+                                     uint32_t* n_mixed) {
+    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < n_b; b0 += gridDim.x * blockDim.x) {  // warp-uniform
+        const uint32_t b = b0 + threadIdx.x;
+        uint32_t bo = b < n_b ? brick[b] : kBrickMixed;
+        bool work = !(bo & kBrickFresh) && !(flags[bo] & F_LEAF);
+        bool cut = false;
+        Agg a;
+        agg_reset(a);
+        if (work) {
+            const int bx = static_cast<int>(b % V.gbx), by = static_cast<int>((b / V.gbx) % V.gby),
+                      bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
+            const double xs[2] = {__ldg(V.cx + bx * kBrick), __ldg(V.cx + bx * kBrick + kBrick - 1)};
+            const double ys[2] = {__ldg(V.cy + by * kBrick), __ldg(V.cy + by * kBrick + kBrick - 1)};
+            const double zs[2] = {__ldg(V.cz + bz * kBrick), __ldg(V.cz + bz * kBrick + kBrick - 1)};
+            uint32_t o = bo;
+            for (;;) {
+                const NodeRec& nd = split[o];
+                const double n0 = nd.n[0], n1 = nd.n[1], n2 = nd.n[2];
+                const double margin = 1e-9 * (fabs(n0) + fabs(n1) + fabs(n2));
+                double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {  // the reference's sp = dot(n, p - pm), left to right
+                    const double sp = (n0 * (xs[c & 1] - nd.pm[0]) + n1 * (ys[(c >> 1) & 1] - nd.pm[1])) +
+                                      n2 * (zs[c >> 2] - nd.pm[2]);
+                    lo = dmin(lo, sp);
+                    hi = dmax(hi, sp);
+                }
+                const bool pos = lo > margin, neg = hi < -margin;
+                if (!pos && !neg) {
+                    cut = true;
+                    bo = o;
+                    break;
+                }
+                const bool take_a = nd.sref_pos ? pos : neg;  // sp >= 0 (sref_pos) or sp <= 0, strictly here
+                o = take_a ? nd.child[0] : nd.child[1];
+                if (flags[o] & F_LEAF) break;
+            }
+            if (cut) {
+                brick[b] = kBrickFresh | bo;
+            } else {
+                brick[b] = o;
+                const BrickStat s = bstat[b];
+                a.sum = s.sum, a.asum = s.asum, a.cnt = s.cnt, a.mn = s.mn, a.mx = s.mx;
+                bo = o;
+            }
+        }
+        warp_flush(st, bo, a, false);
+        list_append(mixed, n_mixed, b, cut);
+    }
+}
+
+// K2 of a round: the voxels of every mixed brick, one warp per brick. A fresh brick's voxels all
+// start from its owner; the others skip voxels whose owner is still a leaf.
+__global__ void __launch_bounds__(kVoxThreads, 4) brick_voxels_kernel(VolView V, uint32_t* brick,
+                                                                      const uint32_t* mixed, const uint32_t* n_mixed,
+                                                                      const NodeRec* split, const uint8_t* flags,
+                                                                      uint32_t* owner, StatsSink st) {
+    const uint32_t n = *n_mixed;
+    const int lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t e = w0; e < n; e += nw) {  // warp-uniform loop
+        const uint32_t b = mixed[e];
+        const uint32_t bo = brick[b];
+        const bool fresh = bo != kBrickMixed;
+        const uint32_t fill = bo & ~kBrickFresh;
+        const int bx = static_cast<int>(b % V.gbx), by = static_cast<int>((b / V.gbx) % V.gby),
+                  bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
+        // lane: rows lane and lane + 32 of the brick's 64 (y, z) rows, 8 voxels each.
+        // All 16 owner words and their flags are loaded before any descent (16
+        // independent loads in flight per lane); a fresh brick's owners are all `fill`.
+        const int x0 = bx * kBrick, nxr = min(kBrick, V.nx - x0);
+        uint32_t own[2][kBrick];
+        uint32_t dirty = 0;  // bit 8h + x
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h, y = by * kBrick + (r & 7), z = bz * kBrick + (r >> 3);
+            const bool row_ok = y < V.ny && z < V.nz;
+            const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
+            if (fresh) {
+#pragma unroll
+                for (int x = 0; x < kBrick; ++x) own[h][x] = fill;
+                if (row_ok) dirty |= ((1u << nxr) - 1u) << (8 * h);
+            } else if (row_ok && nxr == kBrick && ((V.nx & 3) == 0)) {  // 16-B aligned row
+                const uint4 a4 = *reinterpret_cast<const uint4*>(owner + base);
+                const uint4 b4 = *reinterpret_cast<const uint4*>(owner + base + 4);
+                own[h][0] = a4.x, own[h][1] = a4.y, own[h][2] = a4.z, own[h][3] = a4.w;
+                own[h][4] = b4.x, own[h][5] = b4.y, own[h][6] = b4.z, own[h][7] = b4.w;
+            } else {
+#pragma unroll
+                for (int x = 0; x < kBrick; ++x) own[h][x] = row_ok && x < nxr ? owner[base + x] : 0u;
+            }
+        }
+        if (!fresh) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = lane + 32 * h, y = by * kBrick + (r & 7), z = bz * kBrick + (r >> 3);
+                if (y >= V.ny || z >= V.nz) continue;
+#pragma unroll
+                for (int x = 0; x < kBrick; ++x)
+                    if (x < nxr && !(flags[own[h][x]] & F_LEAF)) dirty |= 1u << (8 * h + x);
+            }
+        }
+        VoxLane L;
+        agg_reset(L.a);
+        if (__any_sync(0xffffffffu, dirty != 0)) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t dh = (dirty >> (8 * h)) & 0xffu;
+                if (!dh) continue;
+                const int r = lane + 32 * h, y = by * kBrick + (r & 7), z = bz * kBrick + (r >> 3);
+                const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
+                const double py = __ldg(V.cy + y), pz = __ldg(V.cz + z);
+#pragma unroll
+                for (int x = 0; x < kBrick; ++x) {
+                    if (!((dh >> x) & 1u)) continue;
+                    const uint32_t o = descend(split, flags, own[h][x], mk(__ldg(V.cx + x0 + x), py, pz));
+                    owner[base + x] = o;
+                    vox_add(st, L, o, V.dens[base + x], V, base + x, false);
+                }
+            }
+        }
+        warp_flush(st, L.cur, L.a, false);
+        if (fresh && lane == 0) brick[b] = kBrickMixed;
+    }
+}
+
+// before the payload pass: the owner words of the uniform bricks, so that the
+// owner map alone is authoritative again (one warp per brick)
+__global__ void brick_fill_kernel(VolView V, const uint32_t* brick, uint32_t n_b, uint32_t* owner) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t b = w0; b < n_b; b += nw) {
+        const uint32_t bo = brick[b];
+        if (bo == kBrickMixed) continue;
+        const int bx = static_cast<int>(b % V.gbx), by = static_cast<int>((b / V.gbx) % V.gby),
+                  bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
+        for (int v = lane; v < kBrickVox; v += 32) {
+            const int x = bx * kBrick + (v & (kBrick - 1)), y = by * kBrick + ((v >> kBrickLog) & (kBrick - 1)),
+                      z = bz * kBrick + (v >> (2 * kBrickLog));
+            owner[(static_cast<uint64_t>(z) * V.ny + y) * V.nx + x] = bo;
+        }
+    }
+}
+
 // volume.cpp:47-66
 __device__ double trilinear(const float* data, int nx, int ny, int nz, d3 p) {
     const double fx = p.x * nx - 0.5, fy = p.y * ny - 0.5, fz = p.z * nz - 0.5;
@@ -649,7 +896,7 @@ __device__ Exact exact_scan(const VolView& V, const uint32_t* owner, const tv_te
         for (int j = rlo[1]; j <= rhi[1]; ++j)
             for (int i = rlo[0]; i <= rhi[0]; ++i) {
                 const uint64_t idx = (static_cast<uint64_t>(k) * V.ny + j) * V.nx + i;
-                if (owner[idx] != leaf) continue;
+                if (owner_at(V, owner, i, j, k, idx) != leaf) continue;
                 const double v = V.dens[idx];
                 e.mn = dmin(e.mn, v);
                 e.mx = dmax(e.mx, v);
@@ -1310,13 +1557,14 @@ struct BuildScratch {
     Buf align[3];
     Buf tets, tv4, verts, split, flags, stats, table, vtouch, owner, leaves, sel, tmp, mid, miss_hi, miss_lo,
         miss_idx, miss_hi2, miss_lo2, miss_idx2, head, scan, misc, stripe, fresh, marked, khi, klo, rec, khi2, klo2,
-        rec2, centres;
+        rec2, centres, bricks, bstat, mixed, mixedn;
     template <class F>
     void each(F f) {
         for (auto& b : align) f(b);
         for (Buf* b : {&tets, &tv4, &verts, &split, &flags, &stats, &table, &vtouch, &owner, &leaves, &sel, &tmp,
                        &mid, &miss_hi, &miss_lo, &miss_idx, &miss_hi2, &miss_lo2, &miss_idx2, &head, &scan, &misc,
-                       &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2, &centres})
+                       &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2, &centres, &bricks, &bstat, &mixed,
+                       &mixedn})
             f(*b);
     }
     void release() {
@@ -1455,7 +1703,20 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     double* cxyz = S.centres.as<double>();
     centres_kernel<<<nblk(nx + ny + nz, 256), 256>>>(nx, ny, nz, cxyz);
     CK(cudaGetLastError(), "voxel centres");
-    const VolView V{ch[0], ch[1], ch[2], nx, ny, nz, cxyz, cxyz + nx, cxyz + nx + ny, 1.0 / nx, 1.0 / ny};
+    // voxel bricks (TV_VOX_BRICKS=0: per-voxel ownership sweeps only)
+    static const bool use_bricks = !std::getenv("TV_VOX_BRICKS") || std::atoi(std::getenv("TV_VOX_BRICKS"));
+    const int gbx = (nx + kBrick - 1) / kBrick, gby = (ny + kBrick - 1) / kBrick, gbz = (nz + kBrick - 1) / kBrick;
+    const uint32_t n_bricks = static_cast<uint32_t>(gbx) * gby * gbz;
+    uint32_t* brick_owner = nullptr;
+    if (use_bricks) {
+        TRY(ensure(S.bricks, static_cast<size_t>(n_bricks) * sizeof(uint32_t)));
+        TRY(ensure(S.bstat, static_cast<size_t>(n_bricks) * sizeof(BrickStat)));
+        TRY(ensure(S.mixed, static_cast<size_t>(n_bricks) * sizeof(uint32_t)));
+        TRY(ensure(S.mixedn, 16));
+        brick_owner = S.bricks.as<uint32_t>();
+    }
+    const VolView V{ch[0],      ch[1],      ch[2],         nx,       ny,       nz,          cxyz, cxyz + nx,
+                    cxyz + nx + ny, 1.0 / nx, 1.0 / ny, brick_owner, gbx, gby};
 
     auto grow_tets = [&](size_t need) -> int {
         if (need <= cap_t) return TV_OK;
@@ -1604,14 +1865,28 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             stripe_zero_kernel<<<nblk(fresh_range * kStripes), 256>>>(stripe_b.as<Stats>(), fresh_range * kStripes);
             sink = StatsSink{stats_b.as<Stats>(), stripe_b.as<Stats>(), fresh_lo, fresh_range};
         }
-        if (rounds == 0)
+        if (rounds == 0) {
             vox_stats_kernel<kVoxInit><<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
                                                                     flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
                                                                     sink, 0);
-        else
+            if (use_bricks) {
+                CK(cudaMemset(S.mixedn.p, 0, sizeof(uint32_t)), "bricks");
+                brick_init_kernel<<<vox_blocks, kVoxThreads>>>(V, owner_b.as<uint32_t>(), brick_owner,
+                                                               S.bstat.as<BrickStat>(), S.mixed.as<uint32_t>(),
+                                                               S.mixedn.as<uint32_t>());
+            }
+        } else if (use_bricks) {
+            brick_descend_kernel<<<std::min<unsigned>(nblk(n_bricks, 256), n_sm * 16), 256>>>(
+                V, n_bricks, brick_owner, S.bstat.as<BrickStat>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), sink,
+                S.mixed.as<uint32_t>(), S.mixedn.as<uint32_t>());
+            brick_voxels_kernel<<<vox_blocks, kVoxThreads>>>(V, brick_owner, S.mixed.as<uint32_t>(),
+                                                             S.mixedn.as<uint32_t>(), split_b.as<NodeRec>(),
+                                                             flags_b.as<uint8_t>(), owner_b.as<uint32_t>(), sink);
+        } else {
             vox_stats_kernel<kVoxDescend><<<vox_blocks, kVoxThreads>>>(
                 V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
                 sink, 0);
+        }
         if (sink.n) stripe_combine_kernel<<<nblk(sink.n), 256>>>(sink.stripe, sink.lo, sink.n, stats_b.as<Stats>());
         CK(cudaGetLastError(), "voxel ownership");
         eval_kernel<<<nblk(n_fresh, 128), 128>>>(fresh_b.as<uint32_t>(), n_fresh, V, owner_b.as<uint32_t>(),
@@ -1749,6 +2024,10 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     // Every leaf's density statistics are those of its evaluation round (its
     // voxels have not changed owner since). Temperature / albedo sums need one
     // more pass over the (final) owner map.
+    if (use_bricks && (temp || alb)) {  // the payload sweep reads the owner map alone
+        brick_fill_kernel<<<vox_blocks, kVoxThreads>>>(V, brick_owner, n_bricks, owner_b.as<uint32_t>());
+        CK(cudaGetLastError(), "brick fill");
+    }
     if (temp || alb) {
         stats_zero_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, stats_b.as<Stats>(),
                                                    flags_b.as<uint8_t>());
