@@ -179,7 +179,8 @@ def test_build_scratch_allocators_agree(tv, tmp_path):
     default; TV_BUILD_VMM_TIGHT=1 (granule steps, exactly-sized ranges: every
     growth is a move); TV_BUILD_NO_VMM=1 (cudaMalloc + copy); TV_BUILD_CACHE=0
     (fresh scratch per build); TV_BUILD_POISON=1 (every byte a build has not
-    written reads 0x5A). All give the same grid."""
+    written reads 0x5A); TV_VOX_BRICKS=0 (per-voxel ownership sweeps instead
+    of 8^3 bricks). All give the same grid, byte for byte."""
     import os
     import subprocess
     import sys
@@ -194,7 +195,8 @@ def test_build_scratch_allocators_agree(tv, tmp_path):
     out = {}
     for name, env in [("vmm", {}), ("tight", {"TV_BUILD_VMM_TIGHT": "1"}), ("malloc", {"TV_BUILD_NO_VMM": "1"}),
                       ("nocache", {"TV_BUILD_CACHE": "0"}), ("poison", {"TV_BUILD_POISON": "1"}),
-                      ("poison_tight", {"TV_BUILD_POISON": "1", "TV_BUILD_VMM_TIGHT": "1"})]:
+                      ("poison_tight", {"TV_BUILD_POISON": "1", "TV_BUILD_VMM_TIGHT": "1"}),
+                      ("no_bricks", {"TV_VOX_BRICKS": "0"})]:
         f = str(tmp_path / f"{name}.npz")
         e = dict(os.environ, **env)
         subprocess.run([sys.executable, "-c", code, f], check=True, env=e, timeout=300)
@@ -218,3 +220,31 @@ def test_build_trim_releases_scratch(tv):
     v2, t2, _ = g2.download()
     assert np.array_equal(v1, v2) and np.array_equal(t1.view(np.uint8), t2.view(np.uint8))
     tv.build_trim()
+
+
+def test_build_bricks_match_per_voxel_sweep_cloud256(tv):
+    """At 256^3 most 8^3 bricks stay uniform through the early rounds and
+    descend whole: the grid (pools and stats) must equal the per-voxel
+    ownership sweep's (TV_VOX_BRICKS=0) byte for byte. The CPU oracle is too
+    slow at this size; test_build_cloud64_camera and the others pin the
+    per-voxel sweep to it."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib, torch; sys.path.insert(0, %r); import paper_2506_11510_b200 as tv; "
+            "n = 256; vol = torch.empty(n ** 3, dtype=torch.float32, device='cuda'); "
+            "tv.generate_volume_dev('cloud', n, vol.data_ptr()); "
+            "cam = tv.PinholeCamera((0.5, 0.5, -1.2), (0, 0, 1), (0, 1, 0), 40, 1024, 1024); "
+            "g, s = tv.build_adaptive_grid_dev(vol.data_ptr(), (n, n, n), tv.BuildConfig(1.0, 24, True, 1.0, 16.0), cam); "
+            "v, t, r = g.download(); h = hashlib.sha256(v.tobytes() + t.tobytes() + r.tobytes()).hexdigest(); "
+            "print(h, s.leaf_count, s.rounds, s.criterion_splits, s.propagation_splits)" % root)
+    outs = []
+    for env in ({}, {"TV_VOX_BRICKS": "0"}):
+        p = subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, **env), timeout=300,
+                           capture_output=True, text=True)
+        outs.append(p.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
+    assert int(outs[0].split()[1]) == 3840746
