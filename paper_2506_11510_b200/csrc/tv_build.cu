@@ -609,7 +609,8 @@ __global__ void __launch_bounds__(kVoxThreads, mode == kVoxDescend ? TV_VOX_DESC
 // every voxel of a bisected leaf goes to the same child as its neighbours. The
 // volume is therefore also tiled into 8x8x8 bricks. A brick whose 512 voxels
 // all have one owner keeps that owner in brick_owner[b] (its per-voxel owner
-// words are not maintained) plus its precomputed density statistics. When its
+// words are not maintained) plus its precomputed density statistics; round 0
+// finds those bricks with a corner test against the roots (brick_root_kernel). When its
 // owner is bisected, the brick descends as a whole while the split plane keeps
 // its eight corner centres strictly on one side (margin 1e-9 |n|_1; the side
 // test of every voxel centre inside is then the same, FP rounding included),
@@ -648,10 +649,18 @@ __device__ __forceinline__ void list_append(uint32_t* list, uint32_t* n, uint32_
     if (add) list[base + __popc(m & ((1u << lane) - 1u))] = b;
 }
 
-// after round 0's root scan: one warp per brick; a full brick whose voxels share
-// one owner becomes uniform (with its statistics), every other brick mixed
-__global__ void brick_init_kernel(VolView V, const uint32_t* owner, uint32_t* brick, BrickStat* bstat,
-                                  uint32_t* mixed, uint32_t* n_mixed) {
+// Round 0 with bricks: a full brick whose eight corner centres lie inside the
+// root guessed for its first corner, by more than root_of's 1e-9 acceptance
+// margin on each of the root's planes (plus 1e-9 for rounding), has that root
+// for every voxel: root_of's own test accepts every centre inside, and a
+// centre whose guess differs falls to the reference scan, which can only
+// accept that same root (every other root is violated by more than 1e-12).
+// Such a brick becomes uniform with its statistics added to the root in one
+// step; every other brick takes root_of voxel by voxel and becomes mixed.
+__global__ void __launch_bounds__(kVoxThreads, 3) brick_root_kernel(VolView V, RootScan R, const uint4* verts,
+                                                                    uint32_t* owner, uint32_t* brick,
+                                                                    BrickStat* bstat, StatsSink st, uint32_t* mixed,
+                                                                    uint32_t* n_mixed) {
     const uint32_t n_b = static_cast<uint32_t>(V.gbx) * V.gby * ((V.nz + kBrick - 1) / kBrick);
     const int lane = threadIdx.x & 31;
     const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -660,26 +669,36 @@ __global__ void brick_init_kernel(VolView V, const uint32_t* owner, uint32_t* br
                   bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
         const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick;
         const bool full = x0 + kBrick <= V.nx && y0 + kBrick <= V.ny && z0 + kBrick <= V.nz;
-        uint32_t o0 = kBrickMixed;
-        bool same = full;
-        double sum = 0.0, asum = 0.0;
-        uint32_t mn = 0xffffffffu, mx = 0u;
+        bool uniform = false;
+        int g = 0;
         if (full) {
-            o0 = owner[(static_cast<uint64_t>(z0) * V.ny + y0) * V.nx + x0];
+            g = guess_root(mk(__ldg(V.cx + x0), __ldg(V.cy + y0), __ldg(V.cz + z0)));
+            double worst = -1.0;
+            if (lane < 8) {
+                const d3 p = mk(__ldg(V.cx + x0 + ((lane & 1) ? kBrick - 1 : 0)),
+                                __ldg(V.cy + y0 + ((lane & 2) ? kBrick - 1 : 0)),
+                                __ldg(V.cz + z0 + ((lane & 4) ? kBrick - 1 : 0)));
+                worst = -__longlong_as_double(0x7ff0000000000000ll);
+                for (int slot = 0; slot < 4; ++slot) {
+                    const uint32_t id = (R.nid[g] >> (8 * slot)) & 0xffu;
+                    const d3 w = sub(p, vpos(verts[R.vid[g][(slot + 1) & 3]]));
+                    worst = dmax(worst, ndot(id, w.x, w.y, w.z));
+                }
+            }
+            uniform = __all_sync(0xffffffffu, worst <= -2e-9);
+        }
+        if (uniform) {
+            double sum = 0.0, asum = 0.0;
+            uint32_t mn = 0xffffffffu, mx = 0u;
             for (int v = lane; v < kBrickVox; v += 32) {  // x fastest: lanes read consecutive voxels
                 const int x = x0 + (v & (kBrick - 1)), y = y0 + ((v >> kBrickLog) & (kBrick - 1)),
                           z = z0 + (v >> (2 * kBrickLog));
-                const uint64_t idx = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x;
-                same &= owner[idx] == o0;
-                const float d = V.dens[idx];
+                const float d = V.dens[(static_cast<uint64_t>(z) * V.ny + y) * V.nx + x];
                 sum += static_cast<double>(d);
                 asum += fabs(static_cast<double>(d));
                 mn = min(mn, ord_f(d));
                 mx = max(mx, ord_f(d));
             }
-            same = __all_sync(0xffffffffu, same);
-        }
-        if (same) {
             sum = wsum(sum);
             asum = wsum(asum);
 #pragma unroll
@@ -687,14 +706,39 @@ __global__ void brick_init_kernel(VolView V, const uint32_t* owner, uint32_t* br
                 mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
                 mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             }
+            const uint32_t root = R.id[g];
             if (lane == 0) {
-                brick[b] = o0;
+                brick[b] = root;
                 bstat[b] = BrickStat{sum, asum, static_cast<uint32_t>(kBrickVox), mn, mx, 0u};
             }
-        } else if (lane == 0) {
+            // one lane per brick adds to the root, a different stripe lane per brick
+            if (lane == static_cast<int>(b & 31)) {
+                Agg a;
+                agg_reset(a);
+                a.sum = sum, a.asum = asum, a.cnt = kBrickVox, a.mn = mn, a.mx = mx;
+                stats_atomic_at(st, root, a, false);
+            }
+            continue;
+        }
+        // voxel by voxel (lane: rows lane and lane + 32 of the 64 (y, z) rows)
+        VoxLane L;
+        agg_reset(L.a);
+        const int nxr = min(kBrick, V.nx - x0);
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h, y = y0 + (r & 7), z = z0 + (r >> 3);
+            if (y >= V.ny || z >= V.nz) continue;
+            const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
+            const double py = __ldg(V.cy + y), pz = __ldg(V.cz + z);
+            for (int x = 0; x < nxr; ++x) {
+                const uint32_t o = root_of(R, verts, mk(__ldg(V.cx + x0 + x), py, pz));
+                owner[base + x] = o;
+                vox_add(st, L, o, V.dens[base + x], V, base + x, false);
+            }
+        }
+        warp_flush(st, L.cur, L.a, false);
+        if (lane == 0) {
             brick[b] = kBrickMixed;
-            const uint32_t at = atomicAdd(n_mixed, 1u);
-            mixed[at] = b;
+            mixed[atomicAdd(n_mixed, 1u)] = b;
         }
     }
 }
@@ -1865,16 +1909,15 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             stripe_zero_kernel<<<nblk(fresh_range * kStripes), 256>>>(stripe_b.as<Stats>(), fresh_range * kStripes);
             sink = StatsSink{stats_b.as<Stats>(), stripe_b.as<Stats>(), fresh_lo, fresh_range};
         }
-        if (rounds == 0) {
+        if (rounds == 0 && use_bricks) {
+            CK(cudaMemset(S.mixedn.p, 0, sizeof(uint32_t)), "bricks");
+            brick_root_kernel<<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), owner_b.as<uint32_t>(),
+                                                           brick_owner, S.bstat.as<BrickStat>(), sink,
+                                                           S.mixed.as<uint32_t>(), S.mixedn.as<uint32_t>());
+        } else if (rounds == 0) {
             vox_stats_kernel<kVoxInit><<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
                                                                     flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
                                                                     sink, 0);
-            if (use_bricks) {
-                CK(cudaMemset(S.mixedn.p, 0, sizeof(uint32_t)), "bricks");
-                brick_init_kernel<<<vox_blocks, kVoxThreads>>>(V, owner_b.as<uint32_t>(), brick_owner,
-                                                               S.bstat.as<BrickStat>(), S.mixed.as<uint32_t>(),
-                                                               S.mixedn.as<uint32_t>());
-            }
         } else if (use_bricks) {
             brick_descend_kernel<<<std::min<unsigned>(nblk(n_bricks, 256), n_sm * 16), 256>>>(
                 V, n_bricks, brick_owner, S.bstat.as<BrickStat>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), sink,
