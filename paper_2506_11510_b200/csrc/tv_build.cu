@@ -142,28 +142,44 @@ __device__ __forceinline__ uint64_t coord_hash(uint32_t x, uint32_t y, uint32_t 
     return mix64((static_cast<uint64_t>(x) << 32 | y) ^ mix64(static_cast<uint64_t>(z) + 0x51ull));
 }
 
-__device__ uint32_t hash_find(const uint32_t* table, uint64_t mask, const uint4* verts, uint32_t x, uint32_t y,
+// Open addressing, linear probing, load <= 1/2. A slot holds the vertex id and
+// a 32-bit fingerprint of its coordinates (the hash bits above the slot index):
+// a probe reads the vertex only when the fingerprints match, so a miss (most
+// lookups) costs one or two adjacent slot reads instead of a chain of
+// dependent slot -> vertex loads.
+using HSlot = unsigned long long;
+constexpr HSlot kEmptySlot = ~0ull;
+__device__ __forceinline__ HSlot hslot(uint32_t fp, uint32_t vid) { return static_cast<HSlot>(fp) << 32 | vid; }
+
+__device__ uint32_t hash_find(const HSlot* table, uint64_t mask, const uint4* verts, uint32_t x, uint32_t y,
                               uint32_t z) {
-    uint64_t s = coord_hash(x, y, z) & mask;
+    const uint64_t h = coord_hash(x, y, z);
+    const uint32_t fp = static_cast<uint32_t>(h >> 32);
+    uint64_t s = h & mask;
     for (;;) {
-        const uint32_t v = table[s];
-        if (v == kNone) return kNone;
-        const uint4 q = verts[v];
-        if (q.x == x && q.y == y && q.z == z) return v;
+        const HSlot e = table[s];
+        if (e == kEmptySlot) return kNone;
+        if (static_cast<uint32_t>(e >> 32) == fp) {
+            const uint32_t v = static_cast<uint32_t>(e);
+            const uint4 q = verts[v];
+            if (q.x == x && q.y == y && q.z == z) return v;
+        }
         s = (s + 1) & mask;
     }
 }
 
 // keys are distinct and absent: claim the first empty slot
-__device__ void hash_insert(uint32_t* table, uint64_t mask, uint32_t x, uint32_t y, uint32_t z, uint32_t vid) {
-    uint64_t s = coord_hash(x, y, z) & mask;
+__device__ void hash_insert(HSlot* table, uint64_t mask, uint32_t x, uint32_t y, uint32_t z, uint32_t vid) {
+    const uint64_t h = coord_hash(x, y, z);
+    const HSlot e = hslot(static_cast<uint32_t>(h >> 32), vid);
+    uint64_t s = h & mask;
     for (;;) {
-        if (atomicCAS(table + s, kNone, vid) == kNone) return;
+        if (atomicCAS(table + s, kEmptySlot, e) == kEmptySlot) return;
         s = (s + 1) & mask;
     }
 }
 
-__global__ void hash_rebuild_kernel(uint32_t* table, uint64_t mask, const uint4* verts, uint32_t n) {
+__global__ void hash_rebuild_kernel(HSlot* table, uint64_t mask, const uint4* verts, uint32_t n) {
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const uint4 q = verts[v];
@@ -1051,7 +1067,7 @@ __global__ void eval_kernel(const uint32_t* list, uint32_t n, VolView V, const u
 // midpoint of each marked leaf's refinement edge: existing vertex id, or a
 // "missing" record for sorted dedup
 __global__ void midpoint_kernel(const uint32_t* marked, uint32_t n, const tv_tet* tets, const uint4* verts,
-                                const uint32_t* table, uint64_t mask, uint32_t* mid_vid, uint64_t* miss_hi,
+                                const HSlot* table, uint64_t mask, uint32_t* mid_vid, uint64_t* miss_hi,
                                 uint32_t* miss_lo, uint32_t* miss_idx, uint32_t* n_miss, int* err) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1094,7 +1110,7 @@ __global__ void dedup_heads_kernel(const uint64_t* hi, const uint32_t* lo, uint3
 
 // scan[i] = inclusive count of heads -> vertex id n_v + scan[i] - 1
 __global__ void dedup_assign_kernel(const uint64_t* hi, const uint32_t* lo, const uint32_t* idx, const uint32_t* head,
-                                    const uint32_t* scan, uint32_t n, uint32_t n_v, uint4* verts, uint32_t* table,
+                                    const uint32_t* scan, uint32_t n, uint32_t n_v, uint4* verts, HSlot* table,
                                     uint64_t mask, uint32_t* mid_vid) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -1178,7 +1194,7 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
 // least two vertices touched by that pass (a new midpoint lies on an edge of the
 // bisected tet, whose two endpoints were touched).
 __global__ void hanging_kernel(uint32_t n_t, uint32_t first_new, const uint4* __restrict__ tv4,
-                               const uint4* __restrict__ verts, const uint32_t* __restrict__ table, uint64_t mask,
+                               const uint4* __restrict__ verts, const HSlot* __restrict__ table, uint64_t mask,
                                const uint32_t* __restrict__ vtouch, uint8_t* flags) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_t) return;
@@ -1780,10 +1796,10 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         TRY(ensure(vtouch_b, (nc + 31) / 32 * 4, true));
         size_t slots = 1024;
         while (slots < 2 * nc) slots <<= 1;
-        TRY(ensure(table_b, slots * sizeof(uint32_t)));
-        CK(cudaMemset(table_b.p, 0xff, slots * sizeof(uint32_t)), "hash clear");
+        TRY(ensure(table_b, slots * sizeof(HSlot)));
+        CK(cudaMemset(table_b.p, 0xff, slots * sizeof(HSlot)), "hash clear");
         hmask = slots - 1;
-        hash_rebuild_kernel<<<nblk(n_v), 256>>>(table_b.as<uint32_t>(), hmask, verts_b.as<uint4>(), n_v);
+        hash_rebuild_kernel<<<nblk(n_v), 256>>>(table_b.as<HSlot>(), hmask, verts_b.as<uint4>(), n_v);
         CK(cudaGetLastError(), "hash rebuild");
         cap_v = nc;
         return TV_OK;
@@ -1965,7 +1981,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             TRY(ensure(scan_b, n_marked * sizeof(uint32_t)));
             CK(cudaMemset(d_cnt, 0, sizeof(uint32_t)), "memset");
             midpoint_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, tets_b.as<tv_tet>(),
-                                                     verts_b.as<uint4>(), table_b.as<uint32_t>(), hmask,
+                                                     verts_b.as<uint4>(), table_b.as<HSlot>(), hmask,
                                                      mid_b.as<uint32_t>(), miss_hi_b.as<uint64_t>(),
                                                      miss_lo_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(), d_cnt, d_err);
             CK(cudaGetLastError(), "midpoints");
@@ -2012,7 +2028,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
                 dedup_assign_kernel<<<nblk(n_miss), 256>>>(miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>(),
                                                            miss_idx_b.as<uint32_t>(), head_b.as<uint32_t>(),
                                                            scan_b.as<uint32_t>(), n_miss, n_v, verts_b.as<uint4>(),
-                                                           table_b.as<uint32_t>(), hmask, mid_b.as<uint32_t>());
+                                                           table_b.as<HSlot>(), hmask, mid_b.as<uint32_t>());
                 CK(cudaGetLastError(), "dedup assign");
             }
             if (verbose) ph[0] += since(tp), tp = now();
@@ -2029,7 +2045,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             if (verbose) ph[1] += since(tp), tp = now();
             // hanging test over every tet id, then the marked list (ascending ids)
             hanging_kernel<<<nblk(n_t), 256>>>(n_t, first_new, tv4_b.as<uint4>(), verts_b.as<uint4>(),
-                                               table_b.as<uint32_t>(), hmask, vtouch_b.as<uint32_t>(),
+                                               table_b.as<HSlot>(), hmask, vtouch_b.as<uint32_t>(),
                                                flags_b.as<uint8_t>());
             CK(cudaGetLastError(), "hanging");
             if (verbose) ph[2] += since(tp), tp = now();
