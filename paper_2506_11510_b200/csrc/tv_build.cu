@@ -208,6 +208,7 @@ struct VolView {
     // brick owners (see "voxel bricks"); null: the owner map alone is authoritative
     const uint32_t* brick;
     int gbx, gby;
+    const uint32_t* sub;  // sub-brick owners of mixed bricks (8 per brick)
 };
 
 // the same IEEE division the reference evaluates per voxel, once per coordinate
@@ -648,9 +649,11 @@ struct BrickStat {
 __device__ __forceinline__ uint32_t owner_at(const VolView& V, const uint32_t* owner, int i, int j, int k,
                                              uint64_t idx) {
     if (V.brick) {
-        const uint32_t bo =
-            V.brick[(static_cast<uint64_t>(k >> kBrickLog) * V.gby + (j >> kBrickLog)) * V.gbx + (i >> kBrickLog)];
+        const uint64_t b = (static_cast<uint64_t>(k >> kBrickLog) * V.gby + (j >> kBrickLog)) * V.gbx + (i >> kBrickLog);
+        const uint32_t bo = V.brick[b];
         if (bo != kBrickMixed) return bo;
+        const uint32_t so = V.sub[8 * b + (((i >> 2) & 1) | (((j >> 2) & 1) << 1) | (((k >> 2) & 1) << 2))];
+        if (so != kBrickMixed) return so;
     }
     return owner[idx];
 }
@@ -665,6 +668,33 @@ __device__ __forceinline__ void list_append(uint32_t* list, uint32_t* n, uint32_
     if (add) list[base + __popc(m & ((1u << lane) - 1u))] = b;
 }
 
+// Descent of a box of voxel centres (corner coordinates xs, ys, zs) from node o:
+// true with o = the leaf when every split plane on the way keeps all eight
+// corners strictly on one side (margin 1e-9 |n|_1; sp is linear in p, so every
+// centre inside takes the same branch, rounding included), false with o = the
+// node whose plane cuts the box.
+__device__ __forceinline__ bool box_descend(const NodeRec* split, const uint8_t* flags, uint32_t& o, const double* xs,
+                                            const double* ys, const double* zs) {
+    for (;;) {
+        const NodeRec& nd = split[o];
+        const double n0 = nd.n[0], n1 = nd.n[1], n2 = nd.n[2];
+        const double margin = 1e-9 * (fabs(n0) + fabs(n1) + fabs(n2));
+        double lo = __longlong_as_double(0x7ff0000000000000ll), hi = -lo;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // the reference's sp = dot(n, p - pm), left to right
+            const double sp =
+                (n0 * (xs[c & 1] - nd.pm[0]) + n1 * (ys[(c >> 1) & 1] - nd.pm[1])) + n2 * (zs[c >> 2] - nd.pm[2]);
+            lo = dmin(lo, sp);
+            hi = dmax(hi, sp);
+        }
+        const bool pos = lo > margin, neg = hi < -margin;
+        if (!pos && !neg) return false;
+        const bool take_a = nd.sref_pos ? pos : neg;  // sp >= 0 (sref_pos) or sp <= 0, strictly here
+        o = take_a ? nd.child[0] : nd.child[1];
+        if (flags[o] & F_LEAF) return true;
+    }
+}
+
 // Round 0 with bricks: a full brick whose eight corner centres lie inside the
 // root guessed for its first corner, by more than root_of's 1e-9 acceptance
 // margin on each of the root's planes (plus 1e-9 for rounding), has that root
@@ -674,7 +704,7 @@ __device__ __forceinline__ void list_append(uint32_t* list, uint32_t* n, uint32_
 // Such a brick becomes uniform with its statistics added to the root in one
 // step; every other brick takes root_of voxel by voxel and becomes mixed.
 __global__ void __launch_bounds__(kVoxThreads, 3) brick_root_kernel(VolView V, RootScan R, const uint4* verts,
-                                                                    uint32_t* owner, uint32_t* brick,
+                                                                    uint32_t* owner, uint32_t* brick, uint32_t* subo,
                                                                     BrickStat* bstat, StatsSink st, uint32_t* mixed,
                                                                     uint32_t* n_mixed) {
     const uint32_t n_b = static_cast<uint32_t>(V.gbx) * V.gby * ((V.nz + kBrick - 1) / kBrick);
@@ -752,6 +782,7 @@ __global__ void __launch_bounds__(kVoxThreads, 3) brick_root_kernel(VolView V, R
             }
         }
         warp_flush(st, L.cur, L.a, false);
+        if (lane < 8) subo[8ull * b + lane] = kBrickMixed;
         if (lane == 0) {
             brick[b] = kBrickMixed;
             mixed[atomicAdd(n_mixed, 1u)] = b;
@@ -815,95 +846,170 @@ __global__ void brick_descend_kernel(VolView V, uint32_t n_b, uint32_t* brick, c
     }
 }
 
-// K2 of a round: the voxels of every mixed brick, one warp per brick. A fresh brick's voxels all
-// start from its owner; the others skip voxels whose owner is still a leaf.
-__global__ void __launch_bounds__(kVoxThreads, 4) brick_voxels_kernel(VolView V, uint32_t* brick,
-                                                                      const uint32_t* mixed, const uint32_t* n_mixed,
-                                                                      const NodeRec* split, const uint8_t* flags,
-                                                                      uint32_t* owner, StatsSink st) {
+// K2 of a round: every mixed brick, one warp per brick, in 4x4x4 sub-bricks.
+// A sub-brick with one owner keeps it in sub[8b + s] (its owner words are not
+// maintained) and moves down the tree whole while no plane cuts it, like a
+// brick (lanes 0-7, one sub-brick each); its statistics are computed when its
+// brick is cut (fresh). A cut sub-brick's voxels, and those of sub-bricks that
+// are already per-voxel, are handled one by one: a lane takes rows lane and
+// lane + 32 of the brick's 64 (y, z) rows, loads the owner words and flags of
+// its voxels before any descent, then descends the dirty ones.
+__global__ void __launch_bounds__(kVoxThreads, 4) brick_voxels_kernel(VolView V, uint32_t* brick, uint32_t* subo,
+                                                                      BrickStat* sstat, const uint32_t* mixed,
+                                                                      const uint32_t* n_mixed, const NodeRec* split,
+                                                                      const uint8_t* flags, uint32_t* owner,
+                                                                      StatsSink st) {
     const uint32_t n = *n_mixed;
     const int lane = threadIdx.x & 31;
     const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t e = w0; e < n; e += nw) {  // warp-uniform loop
         const uint32_t b = mixed[e];
         const uint32_t bo = brick[b];
-        const bool fresh = bo != kBrickMixed;
+        const bool fresh = bo != kBrickMixed;  // cut this round: every voxel's owner is `fill`
         const uint32_t fill = bo & ~kBrickFresh;
         const int bx = static_cast<int>(b % V.gbx), by = static_cast<int>((b / V.gbx) % V.gby),
                   bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
-        // lane: rows lane and lane + 32 of the brick's 64 (y, z) rows, 8 voxels each.
-        // All 16 owner words and their flags are loaded before any descent (16
-        // independent loads in flight per lane); a fresh brick's owners are all `fill`.
-        const int x0 = bx * kBrick, nxr = min(kBrick, V.nx - x0);
-        uint32_t own[2][kBrick];
-        uint32_t dirty = 0;  // bit 8h + x
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h, y = by * kBrick + (r & 7), z = bz * kBrick + (r >> 3);
-            const bool row_ok = y < V.ny && z < V.nz;
-            const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
-            if (fresh) {
-#pragma unroll
-                for (int x = 0; x < kBrick; ++x) own[h][x] = fill;
-                if (row_ok) dirty |= ((1u << nxr) - 1u) << (8 * h);
-            } else if (row_ok && nxr == kBrick && ((V.nx & 3) == 0)) {  // 16-B aligned row
-                const uint4 a4 = *reinterpret_cast<const uint4*>(owner + base);
-                const uint4 b4 = *reinterpret_cast<const uint4*>(owner + base + 4);
-                own[h][0] = a4.x, own[h][1] = a4.y, own[h][2] = a4.z, own[h][3] = a4.w;
-                own[h][4] = b4.x, own[h][5] = b4.y, own[h][6] = b4.z, own[h][7] = b4.w;
-            } else {
-#pragma unroll
-                for (int x = 0; x < kBrick; ++x) own[h][x] = row_ok && x < nxr ? owner[base + x] : 0u;
-            }
-        }
-        if (!fresh) {
+        const int x0 = bx * kBrick, y0 = by * kBrick, z0 = bz * kBrick, nxr = min(kBrick, V.nx - x0);
+        uint32_t* sb = subo + 8ull * b;
+        BrickStat* ss = sstat + 8ull * b;
+        // a fresh brick (always full): the statistics of its eight sub-bricks. Lane
+        // rows h = 0, 1 have y = y0 + (lane & 7), z = z0 + (lane >> 3) + 4h, so the
+        // sub-brick of half xh is xh | (lane & 4 ? 2 : 0) | 4h; lanes that share
+        // lane & 4 are summed (xor over lane bits 0, 1, 3, 4)
+        if (fresh) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int r = lane + 32 * h, y = by * kBrick + (r & 7), z = bz * kBrick + (r >> 3);
-                if (y >= V.ny || z >= V.nz) continue;
+                const uint64_t base =
+                    (static_cast<uint64_t>(z0 + (lane >> 3) + 4 * h) * V.ny + (y0 + (lane & 7))) * V.nx + x0;
 #pragma unroll
-                for (int x = 0; x < kBrick; ++x)
-                    if (x < nxr && !(flags[own[h][x]] & F_LEAF)) dirty |= 1u << (8 * h + x);
+                for (int xh = 0; xh < 2; ++xh) {
+                    double sum = 0.0, asum = 0.0;
+                    uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const float d = V.dens[base + 4 * xh + x];
+                        sum += static_cast<double>(d);
+                        asum += fabs(static_cast<double>(d));
+                        mn = min(mn, ord_f(d));
+                        mx = max(mx, ord_f(d));
+                    }
+#pragma unroll
+                    for (int m : {1, 2, 8, 16}) {
+                        sum += __shfl_xor_sync(0xffffffffu, sum, m);
+                        asum += __shfl_xor_sync(0xffffffffu, asum, m);
+                        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, m));
+                        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+                    }
+                    if ((lane & ~4) == 0) ss[xh | ((lane & 4) ? 2 : 0) | (4 * h)] = BrickStat{sum, asum, 64u, mn, mx, 0u};
+                }
             }
+            __syncwarp();
         }
-        VoxLane L;
-        agg_reset(L.a);
-        if (__any_sync(0xffffffffu, dirty != 0)) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t dh = (dirty >> (8 * h)) & 0xffu;
-                if (!dh) continue;
-                const int r = lane + 32 * h, y = by * kBrick + (r & 7), z = bz * kBrick + (r >> 3);
-                const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
-                const double py = __ldg(V.cy + y), pz = __ldg(V.cz + z);
-#pragma unroll
-                for (int x = 0; x < kBrick; ++x) {
-                    if (!((dh >> x) & 1u)) continue;
-                    const uint32_t o = descend(split, flags, own[h][x], mk(__ldg(V.cx + x0 + x), py, pz));
-                    owner[base + x] = o;
-                    vox_add(st, L, o, V.dens[base + x], V, base + x, false);
+        // lanes 0-7: the sub-brick decisions
+        int mode = 0;  // 0 nothing to do, 1 per-voxel (owner words), 2 cut now (every voxel from `ocut`)
+        uint32_t ocut = 0, cur = kNone;
+        Agg a;
+        agg_reset(a);
+        if (lane < 8) {
+            const uint32_t u = fresh ? fill : sb[lane];
+            if (u == kBrickMixed) {
+                mode = 1;
+            } else if (fresh || !(flags[u] & F_LEAF)) {
+                const int sx = x0 + 4 * (lane & 1), sy = y0 + 2 * (lane & 2), sz = z0 + (lane & 4);
+                const double xs[2] = {__ldg(V.cx + sx), __ldg(V.cx + sx + 3)};
+                const double ys[2] = {__ldg(V.cy + sy), __ldg(V.cy + sy + 3)};
+                const double zs[2] = {__ldg(V.cz + sz), __ldg(V.cz + sz + 3)};
+                uint32_t o = u;
+                if (box_descend(split, flags, o, xs, ys, zs)) {
+                    sb[lane] = o;
+                    const BrickStat t = ss[lane];
+                    a.sum = t.sum, a.asum = t.asum, a.cnt = t.cnt, a.mn = t.mn, a.mx = t.mx;
+                    cur = o;
+                } else {
+                    sb[lane] = kBrickMixed;
+                    mode = 2;
+                    ocut = o;
                 }
             }
         }
-        warp_flush(st, L.cur, L.a, false);
+        warp_flush(st, cur, a, false);
+        const uint32_t m1 = __ballot_sync(0xffffffffu, mode == 1) & 0xffu, m2 = __ballot_sync(0xffffffffu, mode == 2) & 0xffu;
+        if (m1 | m2) {
+            uint32_t oc[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) oc[k] = __shfl_sync(0xffffffffu, ocut, k);
+            uint32_t own[2][kBrick];
+            uint32_t dirty = 0;  // bit 8h + x
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = lane + 32 * h, y = y0 + (r & 7), z = z0 + (r >> 3);
+                const bool row_ok = y < V.ny && z < V.nz;
+                const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
+#pragma unroll
+                for (int xh = 0; xh < 2; ++xh) {
+                    const int sbi = xh | ((r & 4) ? 2 : 0) | ((r & 32) ? 4 : 0);
+                    const uint32_t vmask = row_ok ? (((1u << max(0, min(4, nxr - 4 * xh))) - 1u) << (4 * xh)) : 0u;
+                    if ((m2 >> sbi) & 1u) {
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) own[h][4 * xh + x] = oc[sbi];
+                        dirty |= vmask << (8 * h);
+                    } else if (((m1 >> sbi) & 1u) && vmask) {
+                        if (vmask == (0xfu << (4 * xh)) && (V.nx & 3) == 0) {  // 16-B aligned half row
+                            const uint4 q = *reinterpret_cast<const uint4*>(owner + base + 4 * xh);
+                            own[h][4 * xh] = q.x, own[h][4 * xh + 1] = q.y, own[h][4 * xh + 2] = q.z,
+                                        own[h][4 * xh + 3] = q.w;
+                        } else {
+#pragma unroll
+                            for (int x = 0; x < 4; ++x)
+                                own[h][4 * xh + x] = (vmask >> (4 * xh + x)) & 1u ? owner[base + 4 * xh + x] : 0u;
+                        }
+#pragma unroll
+                        for (int x = 0; x < 4; ++x)
+                            if (((vmask >> (4 * xh + x)) & 1u) && !(flags[own[h][4 * xh + x]] & F_LEAF))
+                                dirty |= 1u << (8 * h + 4 * xh + x);
+                    }
+                }
+            }
+            VoxLane L;
+            agg_reset(L.a);
+            if (__any_sync(0xffffffffu, dirty != 0)) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t dh = (dirty >> (8 * h)) & 0xffu;
+                    if (!dh) continue;
+                    const int r = lane + 32 * h, y = y0 + (r & 7), z = z0 + (r >> 3);
+                    const uint64_t base = (static_cast<uint64_t>(z) * V.ny + y) * V.nx + x0;
+                    const double py = __ldg(V.cy + y), pz = __ldg(V.cz + z);
+#pragma unroll
+                    for (int x = 0; x < kBrick; ++x) {
+                        if (!((dh >> x) & 1u)) continue;
+                        const uint32_t o = descend(split, flags, own[h][x], mk(__ldg(V.cx + x0 + x), py, pz));
+                        owner[base + x] = o;
+                        vox_add(st, L, o, V.dens[base + x], V, base + x, false);
+                    }
+                }
+            }
+            warp_flush(st, L.cur, L.a, false);
+        }
         if (fresh && lane == 0) brick[b] = kBrickMixed;
     }
 }
 
 // before the payload pass: the owner words of the uniform bricks, so that the
 // owner map alone is authoritative again (one warp per brick)
-__global__ void brick_fill_kernel(VolView V, const uint32_t* brick, uint32_t n_b, uint32_t* owner) {
+__global__ void brick_fill_kernel(VolView V, const uint32_t* brick, const uint32_t* subo, uint32_t n_b,
+                                  uint32_t* owner) {
     const int lane = threadIdx.x & 31;
     const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t b = w0; b < n_b; b += nw) {
         const uint32_t bo = brick[b];
-        if (bo == kBrickMixed) continue;
         const int bx = static_cast<int>(b % V.gbx), by = static_cast<int>((b / V.gbx) % V.gby),
                   bz = static_cast<int>(b / (static_cast<uint32_t>(V.gbx) * V.gby));
         for (int v = lane; v < kBrickVox; v += 32) {
-            const int x = bx * kBrick + (v & (kBrick - 1)), y = by * kBrick + ((v >> kBrickLog) & (kBrick - 1)),
-                      z = bz * kBrick + (v >> (2 * kBrickLog));
-            owner[(static_cast<uint64_t>(z) * V.ny + y) * V.nx + x] = bo;
+            const int i = v & (kBrick - 1), j = (v >> kBrickLog) & (kBrick - 1), k = v >> (2 * kBrickLog);
+            const uint32_t o = bo != kBrickMixed ? bo : subo[8ull * b + ((i >> 2) | ((j >> 2) << 1) | ((k >> 2) << 2))];
+            if (o == kBrickMixed) continue;  // owner word valid
+            owner[(static_cast<uint64_t>(bz * kBrick + k) * V.ny + (by * kBrick + j)) * V.nx + bx * kBrick + i] = o;
         }
     }
 }
@@ -1617,14 +1723,14 @@ struct BuildScratch {
     Buf align[3];
     Buf tets, tv4, verts, split, flags, stats, table, vtouch, owner, leaves, sel, tmp, mid, miss_hi, miss_lo,
         miss_idx, miss_hi2, miss_lo2, miss_idx2, head, scan, misc, stripe, fresh, marked, khi, klo, rec, khi2, klo2,
-        rec2, centres, bricks, bstat, mixed, mixedn;
+        rec2, centres, bricks, bstat, mixed, mixedn, subs, sstat;
     template <class F>
     void each(F f) {
         for (auto& b : align) f(b);
         for (Buf* b : {&tets, &tv4, &verts, &split, &flags, &stats, &table, &vtouch, &owner, &leaves, &sel, &tmp,
                        &mid, &miss_hi, &miss_lo, &miss_idx, &miss_hi2, &miss_lo2, &miss_idx2, &head, &scan, &misc,
                        &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2, &centres, &bricks, &bstat, &mixed,
-                       &mixedn})
+                       &mixedn, &subs, &sstat})
             f(*b);
     }
     void release() {
@@ -1773,10 +1879,12 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         TRY(ensure(S.bstat, static_cast<size_t>(n_bricks) * sizeof(BrickStat)));
         TRY(ensure(S.mixed, static_cast<size_t>(n_bricks) * sizeof(uint32_t)));
         TRY(ensure(S.mixedn, 16));
+        TRY(ensure(S.subs, static_cast<size_t>(n_bricks) * 8 * sizeof(uint32_t)));
+        TRY(ensure(S.sstat, static_cast<size_t>(n_bricks) * 8 * sizeof(BrickStat)));
         brick_owner = S.bricks.as<uint32_t>();
     }
-    const VolView V{ch[0],      ch[1],      ch[2],         nx,       ny,       nz,          cxyz, cxyz + nx,
-                    cxyz + nx + ny, 1.0 / nx, 1.0 / ny, brick_owner, gbx, gby};
+    const VolView V{ch[0],     ch[1],    ch[2],       nx,  ny,  nz, cxyz, cxyz + nx, cxyz + nx + ny,
+                    1.0 / nx, 1.0 / ny, brick_owner, gbx, gby, use_bricks ? S.subs.as<uint32_t>() : nullptr};
 
     auto grow_tets = [&](size_t need) -> int {
         if (need <= cap_t) return TV_OK;
@@ -1928,7 +2036,8 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         if (rounds == 0 && use_bricks) {
             CK(cudaMemset(S.mixedn.p, 0, sizeof(uint32_t)), "bricks");
             brick_root_kernel<<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), owner_b.as<uint32_t>(),
-                                                           brick_owner, S.bstat.as<BrickStat>(), sink,
+                                                           brick_owner, S.subs.as<uint32_t>(),
+                                                           S.bstat.as<BrickStat>(), sink,
                                                            S.mixed.as<uint32_t>(), S.mixedn.as<uint32_t>());
         } else if (rounds == 0) {
             vox_stats_kernel<kVoxInit><<<vox_blocks, kVoxThreads>>>(V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(),
@@ -1938,9 +2047,9 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             brick_descend_kernel<<<std::min<unsigned>(nblk(n_bricks, 256), n_sm * 16), 256>>>(
                 V, n_bricks, brick_owner, S.bstat.as<BrickStat>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), sink,
                 S.mixed.as<uint32_t>(), S.mixedn.as<uint32_t>());
-            brick_voxels_kernel<<<vox_blocks, kVoxThreads>>>(V, brick_owner, S.mixed.as<uint32_t>(),
-                                                             S.mixedn.as<uint32_t>(), split_b.as<NodeRec>(),
-                                                             flags_b.as<uint8_t>(), owner_b.as<uint32_t>(), sink);
+            brick_voxels_kernel<<<vox_blocks, kVoxThreads>>>(
+                V, brick_owner, S.subs.as<uint32_t>(), S.sstat.as<BrickStat>(), S.mixed.as<uint32_t>(),
+                S.mixedn.as<uint32_t>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(), sink);
         } else {
             vox_stats_kernel<kVoxDescend><<<vox_blocks, kVoxThreads>>>(
                 V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
@@ -2084,7 +2193,8 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     // voxels have not changed owner since). Temperature / albedo sums need one
     // more pass over the (final) owner map.
     if (use_bricks && (temp || alb)) {  // the payload sweep reads the owner map alone
-        brick_fill_kernel<<<vox_blocks, kVoxThreads>>>(V, brick_owner, n_bricks, owner_b.as<uint32_t>());
+        brick_fill_kernel<<<vox_blocks, kVoxThreads>>>(V, brick_owner, S.subs.as<uint32_t>(), n_bricks,
+                                                       owner_b.as<uint32_t>());
         CK(cudaGetLastError(), "brick fill");
     }
     if (temp || alb) {
