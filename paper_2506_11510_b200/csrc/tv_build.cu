@@ -646,6 +646,65 @@ struct BrickStat {
     uint32_t cnt, mn, mx, pad;
 };
 
+// Bricks that may hold a voxel whose owner a closure pass bisects: the bricks
+// of the bisected tet's voxel bounding box (a voxel centre lies inside its
+// owner). The next round's mixed-brick pass visits only those. A tet whose box
+// spans more than kMarkMax bricks marks its super-bricks (8x8x8 bricks) in a
+// second bitmap instead, and one spanning more than kMarkMax super-bricks the
+// all-bricks word.
+struct BrickMark {
+    uint32_t* bits;   // 1 bit per brick; null: no bricks
+    uint32_t* sbits;  // 1 bit per super-brick, then the all-bricks word
+    uint32_t n_swords;
+    int nx, ny, nz, gbx, gby, gsx, gsy;
+};
+constexpr int kMarkMax = 256;
+
+__device__ __forceinline__ bool brick_marked(const BrickMark& M, uint32_t b, int gbx, int gby) {
+    if ((M.bits[b >> 5] >> (b & 31)) & 1u) return true;
+    const uint32_t bx = b % gbx, by = (b / gbx) % gby, bz = b / (static_cast<uint32_t>(gbx) * gby);
+    const uint32_t sb = ((bz >> 3) * M.gsy + (by >> 3)) * M.gsx + (bx >> 3);
+    return (M.sbits[sb >> 5] >> (sb & 31)) & 1u;
+}
+
+__device__ void mark_bricks(const BrickMark& M, const uint4* verts, const tv_tet& t) {
+    if (!M.bits) return;
+    double lo[3] = {1.0, 1.0, 1.0}, hi[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < 4; ++k) {
+        const d3 c = vpos(verts[t.verts[k]]);
+        lo[0] = dmin(lo[0], c.x), lo[1] = dmin(lo[1], c.y), lo[2] = dmin(lo[2], c.z);
+        hi[0] = dmax(hi[0], c.x), hi[1] = dmax(hi[1], c.y), hi[2] = dmax(hi[2], c.z);
+    }
+    const int dims[3] = {M.nx, M.ny, M.nz};
+    int b0[3], b1[3];
+    uint64_t count = 1, scount = 1;
+    for (int a = 0; a < 3; ++a) {  // centre (i + 0.5) / n in [lo, hi], widened by one voxel
+        const int i0 = max(0, static_cast<int>(floor(lo[a] * dims[a] - 0.5)) - 1);
+        const int i1 = min(dims[a] - 1, static_cast<int>(ceil(hi[a] * dims[a] - 0.5)) + 1);
+        b0[a] = i0 >> kBrickLog, b1[a] = i1 >> kBrickLog;
+        count *= static_cast<uint64_t>(max(0, b1[a] - b0[a] + 1));
+        scount *= static_cast<uint64_t>(max(0, (b1[a] >> 3) - (b0[a] >> 3) + 1));
+    }
+    if (count <= kMarkMax) {
+        for (int z = b0[2]; z <= b1[2]; ++z)
+            for (int y = b0[1]; y <= b1[1]; ++y)
+                for (int x = b0[0]; x <= b1[0]; ++x) {
+                    const uint32_t b = (static_cast<uint32_t>(z) * M.gby + y) * M.gbx + x;
+                    atomicOr(M.bits + (b >> 5), 1u << (b & 31));
+                }
+    } else if (scount <= kMarkMax) {
+        for (int z = b0[2] >> 3; z <= (b1[2] >> 3); ++z)
+            for (int y = b0[1] >> 3; y <= (b1[1] >> 3); ++y)
+                for (int x = b0[0] >> 3; x <= (b1[0] >> 3); ++x) {
+                    const uint32_t sb = (static_cast<uint32_t>(z) * M.gsy + y) * M.gsx + x;
+                    atomicOr(M.sbits + (sb >> 5), 1u << (sb & 31));
+                }
+    } else {
+        atomicOr(M.sbits + M.n_swords - 1, 1u);
+    }
+}
+
+
 __device__ __forceinline__ uint32_t owner_at(const VolView& V, const uint32_t* owner, int i, int j, int k,
                                              uint64_t idx) {
     if (V.brick) {
@@ -858,12 +917,14 @@ __global__ void __launch_bounds__(kVoxThreads, 4) brick_voxels_kernel(VolView V,
                                                                       BrickStat* sstat, const uint32_t* mixed,
                                                                       const uint32_t* n_mixed, const NodeRec* split,
                                                                       const uint8_t* flags, uint32_t* owner,
-                                                                      StatsSink st) {
+                                                                      StatsSink st, BrickMark bm) {
     const uint32_t n = *n_mixed;
     const int lane = threadIdx.x & 31;
     const uint32_t w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const bool all = !bm.bits || (bm.sbits[bm.n_swords - 1] & 1u);
     for (uint32_t e = w0; e < n; e += nw) {  // warp-uniform loop
         const uint32_t b = mixed[e];
+        if (!all && !brick_marked(bm, b, V.gbx, V.gby)) continue;  // no owner here was bisected
         const uint32_t bo = brick[b];
         const bool fresh = bo != kBrickMixed;  // cut this round: every voxel's owner is `fill`
         const uint32_t fill = bo & ~kBrickFresh;
@@ -1234,11 +1295,12 @@ __global__ void dedup_assign_kernel(const uint64_t* hi, const uint32_t* lo, cons
 // n_t + 2i, n_t + 2i + 1 in marked-list (ascending id) order.
 __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, tv_tet* tets, uint4* tv4,
                               const uint4* verts, const uint32_t* mid_vid, NodeRec* split, uint8_t* flags,
-                              uint32_t* vtouch, int max_level, int* err) {
+                              uint32_t* vtouch, int max_level, int* err, BrickMark bm) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t t = marked[i];
     const tv_tet parent = tets[t];
+    mark_bricks(bm, verts, parent);
     if (parent.level >= max_level) atomicOr(err, E_LEVEL);  // MaxLevelExceeded (tet_grid.cpp:342)
     int s0, s1;
     refinement_slots(parent, verts, s0, s1);
@@ -1723,14 +1785,14 @@ struct BuildScratch {
     Buf align[3];
     Buf tets, tv4, verts, split, flags, stats, table, vtouch, owner, leaves, sel, tmp, mid, miss_hi, miss_lo,
         miss_idx, miss_hi2, miss_lo2, miss_idx2, head, scan, misc, stripe, fresh, marked, khi, klo, rec, khi2, klo2,
-        rec2, centres, bricks, bstat, mixed, mixedn, subs, sstat;
+        rec2, centres, bricks, bstat, mixed, mixedn, subs, sstat, bmark;
     template <class F>
     void each(F f) {
         for (auto& b : align) f(b);
         for (Buf* b : {&tets, &tv4, &verts, &split, &flags, &stats, &table, &vtouch, &owner, &leaves, &sel, &tmp,
                        &mid, &miss_hi, &miss_lo, &miss_idx, &miss_hi2, &miss_lo2, &miss_idx2, &head, &scan, &misc,
                        &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2, &centres, &bricks, &bstat, &mixed,
-                       &mixedn, &subs, &sstat})
+                       &mixedn, &subs, &sstat, &bmark})
             f(*b);
     }
     void release() {
@@ -1883,6 +1945,17 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         TRY(ensure(S.sstat, static_cast<size_t>(n_bricks) * 8 * sizeof(BrickStat)));
         brick_owner = S.bricks.as<uint32_t>();
     }
+    // brick marks: n_bricks bits, then one bit per super-brick (8^3 bricks) and the all-bricks word
+    const int gsx = (gbx + 7) / 8, gsy = (gby + 7) / 8, gsz = (gbz + 7) / 8;
+    const uint32_t bwords = n_bricks / 32 + 1, swords = static_cast<uint32_t>(gsx) * gsy * gsz / 32 + 2;
+    const uint32_t mark_words = bwords + swords;
+    if (use_bricks) {
+        TRY(ensure(S.bmark, static_cast<size_t>(mark_words) * sizeof(uint32_t)));
+        CK(cudaMemset(S.bmark.p, 0, mark_words * sizeof(uint32_t)), "brick marks");
+    }
+    const BrickMark bmark{use_bricks ? S.bmark.as<uint32_t>() : nullptr,
+                          use_bricks ? S.bmark.as<uint32_t>() + bwords : nullptr,
+                          swords, nx, ny, nz, gbx, gby, gsx, gsy};
     const VolView V{ch[0],     ch[1],    ch[2],       nx,  ny,  nz, cxyz, cxyz + nx, cxyz + nx + ny,
                     1.0 / nx, 1.0 / ny, brick_owner, gbx, gby, use_bricks ? S.subs.as<uint32_t>() : nullptr};
 
@@ -2049,7 +2122,10 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
                 S.mixed.as<uint32_t>(), S.mixedn.as<uint32_t>());
             brick_voxels_kernel<<<vox_blocks, kVoxThreads>>>(
                 V, brick_owner, S.subs.as<uint32_t>(), S.sstat.as<BrickStat>(), S.mixed.as<uint32_t>(),
-                S.mixedn.as<uint32_t>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(), sink);
+                S.mixedn.as<uint32_t>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(), sink,
+                bmark);
+            // the marks of the coming closure start empty
+            CK(cudaMemsetAsync(S.bmark.p, 0, mark_words * sizeof(uint32_t), 0), "brick marks");
         } else {
             vox_stats_kernel<kVoxDescend><<<vox_blocks, kVoxThreads>>>(
                 V, R, verts_b.as<uint4>(), split_b.as<NodeRec>(), flags_b.as<uint8_t>(), owner_b.as<uint32_t>(),
@@ -2145,7 +2221,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             bisect_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, n_t, tets_b.as<tv_tet>(),
                                                    tv4_b.as<uint4>(), verts_b.as<uint4>(), mid_b.as<uint32_t>(),
                                                    split_b.as<NodeRec>(), flags_b.as<uint8_t>(),
-                                                   vtouch_b.as<uint32_t>(), grid_max_level, d_err);
+                                                   vtouch_b.as<uint32_t>(), grid_max_level, d_err, bmark);
             CK(cudaGetLastError(), "bisect");
             const uint32_t first_new = n_t;
             n_t += 2 * n_marked;
