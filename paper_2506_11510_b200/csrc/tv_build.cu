@@ -1233,9 +1233,18 @@ __global__ void eval_kernel(const uint32_t* list, uint32_t n, VolView V, const u
 
 // midpoint of each marked leaf's refinement edge: existing vertex id, or a
 // "missing" record for sorted dedup
+// Missing midpoints of a closure pass get new vertex ids without a sort. Every
+// marked leaf whose refinement-edge midpoint is not a vertex claims the
+// midpoint in a pending table (slot = coordinate fingerprint << 32 | marked
+// index; the smallest marked index wins through atomicMin), the winners are
+// counted by a scan in marked-list order, and the midpoint gets id n_v + its
+// winner's rank. The marked list is in ascending tet id order, so the ids are
+// deterministic; like every GPU id they are an allocation artefact (F3).
+constexpr uint32_t kMidMissing = 0xfffffffeu;
+
 __global__ void midpoint_kernel(const uint32_t* marked, uint32_t n, const tv_tet* tets, const uint4* verts,
-                                const HSlot* table, uint64_t mask, uint32_t* mid_vid, uint64_t* miss_hi,
-                                uint32_t* miss_lo, uint32_t* miss_idx, uint32_t* n_miss, int* err) {
+                                const HSlot* table, uint64_t mask, uint32_t* mid_vid, uint64_t* khi, uint32_t* klo,
+                                HSlot* pend, uint64_t pmask, int* err) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const tv_tet tt = tets[marked[i]];
@@ -1252,42 +1261,88 @@ __global__ void midpoint_kernel(const uint32_t* marked, uint32_t n, const tv_tet
     const uint32_t mx = static_cast<uint32_t>(sx / 2), my = static_cast<uint32_t>(sy / 2),
                    mz = static_cast<uint32_t>(sz / 2);
     const uint32_t v = hash_find(table, mask, verts, mx, my, mz);
-    mid_vid[i] = v;
-    // missing midpoints claim their slots with one atomic per warp
-    const unsigned act = __activemask();
-    const unsigned m = __ballot_sync(act, v == kNone);
-    if (!m) return;
-    const int leader = __ffs(m) - 1, lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(n_miss, static_cast<uint32_t>(__popc(m)));
-    base = __shfl_sync(act, base, leader);
-    if (v == kNone) {
-        const uint32_t k = base + __popc(m & ((1u << lane) - 1u));
-        miss_hi[k] = static_cast<uint64_t>(mx) << 25 | my;
-        miss_lo[k] = mz;
-        miss_idx[k] = i;
+    if (v != kNone) {
+        mid_vid[i] = v;
+        return;
+    }
+    mid_vid[i] = kMidMissing;
+    const uint64_t kh = static_cast<uint64_t>(mx) << 25 | my;
+    khi[i] = kh;
+    klo[i] = mz;
+    __threadfence();  // the key is visible before the claim that names it
+    const uint64_t h = coord_hash(mx, my, mz);
+    const uint32_t fp = static_cast<uint32_t>(h >> 32);
+    const HSlot me = hslot(fp, i);
+    for (uint64_t s = h & pmask, k = 0;; s = (s + 1) & pmask) {
+        if (k++ > pmask) {  // full table: cannot happen at load <= 1/2
+            atomicOr(err, E_MIDPOINT);
+            return;
+        }
+        const HSlot e = atomicCAS(pend + s, kEmptySlot, me);
+        if (e == kEmptySlot) return;  // first claim
+        if (static_cast<uint32_t>(e >> 32) == fp) {
+            const uint32_t j = static_cast<uint32_t>(e);
+            if (__ldcg(khi + j) == kh && __ldcg(klo + j) == mz) {
+                atomicMin(pend + s, me);  // same midpoint: the smaller marked index wins
+                return;
+            }
+        }
     }
 }
 
-__global__ void dedup_heads_kernel(const uint64_t* hi, const uint32_t* lo, uint32_t n, uint32_t* head) {
+// each missing midpoint's winner and slot; flag = 1 for winners
+__global__ void midpoint_win_kernel(const uint32_t* mid_vid, uint32_t n, const uint64_t* khi, const uint32_t* klo,
+                                    const HSlot* pend, uint64_t pmask, uint32_t* win, uint32_t* slot,
+                                    uint32_t* flag) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    head[i] = (i == 0 || hi[i] != hi[i - 1] || lo[i] != lo[i - 1]) ? 1u : 0u;
+    if (mid_vid[i] != kMidMissing) {
+        flag[i] = 0;
+        return;
+    }
+    const uint64_t kh = khi[i];
+    const uint32_t kz = klo[i];
+    const uint64_t h = coord_hash(static_cast<uint32_t>(kh >> 25), static_cast<uint32_t>(kh & 0x1ffffffull), kz);
+    const uint32_t fp = static_cast<uint32_t>(h >> 32);
+    for (uint64_t s = h & pmask, k = 0;; s = (s + 1) & pmask) {
+        if (k++ > pmask) {  // not found (an error was flagged in the claim)
+            win[i] = kNone;
+            flag[i] = 0;
+            return;
+        }
+        const HSlot e = pend[s];
+        if (static_cast<uint32_t>(e >> 32) == fp) {
+            const uint32_t j = static_cast<uint32_t>(e);
+            if (khi[j] == kh && klo[j] == kz) {
+                win[i] = j;
+                slot[i] = static_cast<uint32_t>(s);
+                flag[i] = j == i ? 1u : 0u;
+                return;
+            }
+        }
+    }
 }
 
-// scan[i] = inclusive count of heads -> vertex id n_v + scan[i] - 1
-__global__ void dedup_assign_kernel(const uint64_t* hi, const uint32_t* lo, const uint32_t* idx, const uint32_t* head,
-                                    const uint32_t* scan, uint32_t n, uint32_t n_v, uint4* verts, HSlot* table,
-                                    uint64_t mask, uint32_t* mid_vid) {
+// scan = inclusive count of winners in marked order: midpoint id n_v + scan[winner] - 1;
+// winners write the vertex, insert it and free their pending slot
+__global__ void midpoint_assign_kernel(uint32_t* mid_vid, uint32_t n, const uint64_t* khi, const uint32_t* klo,
+                                       const uint32_t* win, const uint32_t* slot, const uint32_t* scan, uint32_t n_v,
+                                       uint4* verts, HSlot* table, uint64_t mask, HSlot* pend) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t vid = n_v + scan[i] - 1;
-    mid_vid[idx[i]] = vid;
-    if (head[i]) {
-        const uint32_t x = static_cast<uint32_t>(hi[i] >> 25), y = static_cast<uint32_t>(hi[i] & 0x1ffffffull),
-                       z = lo[i];
+    if (i >= n || mid_vid[i] != kMidMissing) return;
+    const uint32_t w = win[i];
+    if (w == kNone) {  // failed claim (flagged)
+        mid_vid[i] = kNone;
+        return;
+    }
+    const uint32_t vid = n_v + scan[w] - 1;
+    mid_vid[i] = vid;
+    if (w == i) {
+        const uint32_t x = static_cast<uint32_t>(khi[i] >> 25), y = static_cast<uint32_t>(khi[i] & 0x1ffffffull),
+                       z = klo[i];
         verts[vid] = make_uint4(x, y, z, 0);
         hash_insert(table, mask, x, y, z, vid);
+        pend[slot[i]] = kEmptySlot;
     }
 }
 
@@ -1398,7 +1453,7 @@ struct FlagBit {
 // the pass, [1] leaves marked for the next pass, [2] error bits
 __global__ void pass_state_kernel(const uint32_t* scan, uint32_t n_miss, const uint32_t* n_marked, const int* err,
                                   uint32_t* out) {
-    out[0] = n_miss ? scan[n_miss - 1] : 0u;
+    out[0] = n_miss ? scan[n_miss - 1] : 0u;  // new vertices: winners among the pass's marked leaves
     out[1] = *n_marked;
     out[2] = static_cast<uint32_t>(*err);
 }
@@ -1517,21 +1572,6 @@ __global__ void face_pair_kernel(const uint64_t* khi, const uint32_t* klo, const
     tets[t].neighbors[slot] = other;
 }
 
-// keys of the refinement-edge midpoint for marked[idx[p]] in position p
-__global__ void regather_kernel(const uint32_t* idx, const uint32_t* marked, uint32_t n, const tv_tet* tets,
-                                const uint4* verts, uint64_t* hi, uint32_t* lo) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const tv_tet tt = tets[marked[idx[p]]];
-    int s0, s1;
-    refinement_slots(tt, verts, s0, s1);
-    const uint4 a = verts[tt.verts[s0]], b = verts[tt.verts[s1]];
-    const uint32_t mx = static_cast<uint32_t>((static_cast<uint64_t>(a.x) + b.x) / 2),
-                   my = static_cast<uint32_t>((static_cast<uint64_t>(a.y) + b.y) / 2),
-                   mz = static_cast<uint32_t>((static_cast<uint64_t>(a.z) + b.z) / 2);
-    hi[p] = static_cast<uint64_t>(mx) << 25 | my;
-    lo[p] = mz;
-}
 
 // face key of face record rec[p] (4 * leaf-list index + slot)
 __global__ void gather_face_hi_kernel(const uint32_t* rec, uint64_t n, const uint32_t* leaves, const tv_tet* tets,
@@ -1785,14 +1825,14 @@ struct BuildScratch {
     Buf align[3];
     Buf tets, tv4, verts, split, flags, stats, table, vtouch, owner, leaves, sel, tmp, mid, miss_hi, miss_lo,
         miss_idx, miss_hi2, miss_lo2, miss_idx2, head, scan, misc, stripe, fresh, marked, khi, klo, rec, khi2, klo2,
-        rec2, centres, bricks, bstat, mixed, mixedn, subs, sstat, bmark;
+        rec2, centres, bricks, bstat, mixed, mixedn, subs, sstat, bmark, pend;
     template <class F>
     void each(F f) {
         for (auto& b : align) f(b);
         for (Buf* b : {&tets, &tv4, &verts, &split, &flags, &stats, &table, &vtouch, &owner, &leaves, &sel, &tmp,
                        &mid, &miss_hi, &miss_lo, &miss_idx, &miss_hi2, &miss_lo2, &miss_idx2, &head, &scan, &misc,
                        &stripe, &fresh, &marked, &khi, &klo, &rec, &khi2, &klo2, &rec2, &centres, &bricks, &bstat, &mixed,
-                       &mixedn, &subs, &sstat, &bmark})
+                       &mixedn, &subs, &sstat, &bmark, &pend})
             f(*b);
     }
     void release() {
@@ -2061,6 +2101,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     };
 
     uint64_t crit = 0, bisections = 0, passes = 0, replays = 0;
+    bool pend_clean = false;  // the pending-midpoint table has been cleared in this build
     int rounds = 0;
     uint32_t n_fresh = 24, n_marked = 0, n_leaves = 24;
     uint32_t fresh_lo = 0;                    // the fresh leaves' ids lie in [fresh_lo, n_t)
@@ -2159,63 +2200,51 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             TRY(ensure(miss_hi_b, n_marked * sizeof(uint64_t)));
             TRY(ensure(miss_lo_b, n_marked * sizeof(uint32_t)));
             TRY(ensure(miss_idx_b, n_marked * sizeof(uint32_t)));
-            TRY(ensure(miss_hi2_b, n_marked * sizeof(uint64_t)));
-            TRY(ensure(miss_lo2_b, n_marked * sizeof(uint32_t)));
             TRY(ensure(miss_idx2_b, n_marked * sizeof(uint32_t)));
             TRY(ensure(head_b, n_marked * sizeof(uint32_t)));
             TRY(ensure(scan_b, n_marked * sizeof(uint32_t)));
-            CK(cudaMemset(d_cnt, 0, sizeof(uint32_t)), "memset");
+            {
+                // pending-claim table: a power of two >= 2 n_marked slots, empty between passes
+                size_t pslots = 1024;
+                while (pslots < 2ull * n_marked) pslots <<= 1;
+                if (S.pend.bytes < pslots * sizeof(HSlot)) {
+                    const size_t had = pend_clean ? S.pend.bytes : 0;
+                    TRY(ensure(S.pend, pslots * sizeof(HSlot)));
+                    CK(cudaMemset(static_cast<char*>(S.pend.p) + had, 0xff, S.pend.bytes - had), "pending clear");
+                } else if (!pend_clean) {  // first pass of this build: the table may hold anything
+                    CK(cudaMemset(S.pend.p, 0xff, S.pend.bytes), "pending clear");
+                }
+                pend_clean = true;  // every pass frees the slots it claims
+            }
+            const uint64_t pmask = S.pend.bytes / sizeof(HSlot);  // every slot is used: mask = slots - 1
+            uint64_t pm = 1;
+            while (pm * 2 <= pmask) pm *= 2;
             midpoint_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, tets_b.as<tv_tet>(),
                                                      verts_b.as<uint4>(), table_b.as<HSlot>(), hmask,
                                                      mid_b.as<uint32_t>(), miss_hi_b.as<uint64_t>(),
-                                                     miss_lo_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(), d_cnt, d_err);
+                                                     miss_lo_b.as<uint32_t>(), S.pend.as<HSlot>(), pm - 1, d_err);
             CK(cudaGetLastError(), "midpoints");
-            uint32_t n_miss = 0;
-            CK(cudaMemcpy(&n_miss, d_cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost), "miss count");
-            if (n_miss) {
-                // stable LSD: by z, then by (x, y); payload = marked index
-                size_t tb1 = 0, tb2 = 0, tb3 = 0;
-                CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, miss_lo_b.as<uint32_t>(), miss_lo2_b.as<uint32_t>(),
-                                                   miss_idx_b.as<uint32_t>(), miss_idx2_b.as<uint32_t>(),
-                                                   static_cast<int>(n_miss), 0, 25),
-                   "sort sizing");
-                CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, miss_hi_b.as<uint64_t>(), miss_hi2_b.as<uint64_t>(),
-                                                   miss_idx2_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(),
-                                                   static_cast<int>(n_miss), 0, 50),
-                   "sort sizing");
+            midpoint_win_kernel<<<nblk(n_marked), 256>>>(mid_b.as<uint32_t>(), n_marked, miss_hi_b.as<uint64_t>(),
+                                                         miss_lo_b.as<uint32_t>(), S.pend.as<HSlot>(), pm - 1,
+                                                         miss_idx_b.as<uint32_t>(), miss_idx2_b.as<uint32_t>(),
+                                                         head_b.as<uint32_t>());
+            {
+                size_t tb3 = 0;
                 CK(cub::DeviceScan::InclusiveSum(nullptr, tb3, head_b.as<uint32_t>(), scan_b.as<uint32_t>(),
-                                                 static_cast<int>(n_miss)),
+                                                 static_cast<int>(n_marked)),
                    "scan sizing");
-                TRY(ensure(tmp_b, std::max(tb1, std::max(tb2, tb3))));
-                CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb1, miss_lo_b.as<uint32_t>(), miss_lo2_b.as<uint32_t>(),
-                                                   miss_idx_b.as<uint32_t>(), miss_idx2_b.as<uint32_t>(),
-                                                   static_cast<int>(n_miss), 0, 25),
-                   "sort lo");
-                // recompute the keys in z-sorted order (position p <- marked[idx2[p]])
-                regather_kernel<<<nblk(n_miss), 256>>>(miss_idx2_b.as<uint32_t>(), marked_b.as<uint32_t>(), n_miss,
-                                                       tets_b.as<tv_tet>(), verts_b.as<uint4>(),
-                                                       miss_hi_b.as<uint64_t>(), miss_lo_b.as<uint32_t>());
-                CK(cudaGetLastError(), "regather");
-                CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb2, miss_hi_b.as<uint64_t>(), miss_hi2_b.as<uint64_t>(),
-                                                   miss_idx2_b.as<uint32_t>(), miss_idx_b.as<uint32_t>(),
-                                                   static_cast<int>(n_miss), 0, 50),
-                   "sort hi");
-                regather_kernel<<<nblk(n_miss), 256>>>(miss_idx_b.as<uint32_t>(), marked_b.as<uint32_t>(), n_miss,
-                                                       tets_b.as<tv_tet>(), verts_b.as<uint4>(),
-                                                       miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>());
-                CK(cudaGetLastError(), "regather");
-                dedup_heads_kernel<<<nblk(n_miss), 256>>>(miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>(), n_miss,
-                                                          head_b.as<uint32_t>());
+                TRY(ensure(tmp_b, tb3));
                 CK(cub::DeviceScan::InclusiveSum(tmp_b.p, tb3, head_b.as<uint32_t>(), scan_b.as<uint32_t>(),
-                                                 static_cast<int>(n_miss)),
+                                                 static_cast<int>(n_marked)),
                    "scan");
-                // capacity for n_v + n_marked vertices is already mapped (n_new <= n_miss)
-                dedup_assign_kernel<<<nblk(n_miss), 256>>>(miss_hi2_b.as<uint64_t>(), miss_lo2_b.as<uint32_t>(),
-                                                           miss_idx_b.as<uint32_t>(), head_b.as<uint32_t>(),
-                                                           scan_b.as<uint32_t>(), n_miss, n_v, verts_b.as<uint4>(),
-                                                           table_b.as<HSlot>(), hmask, mid_b.as<uint32_t>());
-                CK(cudaGetLastError(), "dedup assign");
             }
+            // capacity for n_v + n_marked vertices is already mapped (new vertices <= n_marked)
+            midpoint_assign_kernel<<<nblk(n_marked), 256>>>(
+                mid_b.as<uint32_t>(), n_marked, miss_hi_b.as<uint64_t>(), miss_lo_b.as<uint32_t>(),
+                miss_idx_b.as<uint32_t>(), miss_idx2_b.as<uint32_t>(), scan_b.as<uint32_t>(), n_v,
+                verts_b.as<uint4>(), table_b.as<HSlot>(), hmask, S.pend.as<HSlot>());
+            CK(cudaGetLastError(), "midpoint ids");
+            const uint32_t n_pass = n_marked;
             if (verbose) ph[0] += since(tp), tp = now();
             CK(cudaMemset(vtouch_b.p, 0, (n_v + 31) / 32 * 4), "vtouch");  // bisect touches existing vertices only
             bisect_kernel<<<nblk(n_marked), 256>>>(marked_b.as<uint32_t>(), n_marked, n_t, tets_b.as<tv_tet>(),
@@ -2235,7 +2264,7 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             CK(cudaGetLastError(), "hanging");
             if (verbose) ph[2] += since(tp), tp = now();
             TRY(select_tets(F_MARK, marked_b, nullptr));
-            pass_state_kernel<<<1, 1>>>(scan_b.as<uint32_t>(), n_miss, d_cnt, d_err, d_state);
+            pass_state_kernel<<<1, 1>>>(scan_b.as<uint32_t>(), n_pass, d_cnt, d_err, d_state);
             uint32_t hs[3];
             CK(cudaMemcpy(hs, d_state, sizeof(hs), cudaMemcpyDeviceToHost), "pass state");
             n_v += hs[0];
