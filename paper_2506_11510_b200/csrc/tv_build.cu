@@ -1534,7 +1534,7 @@ __global__ void payload_kernel(const uint32_t* list, uint32_t n, VolView V, cons
 
 // face records for neighbour pairing: key = sorted vertex triple
 __global__ void face_keys_kernel(const uint32_t* leaves, uint32_t n, const tv_tet* tets, uint64_t* khi, uint32_t* klo,
-                                 uint32_t* rec) {
+                                 uint32_t* rec, int vb) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t t = leaves[i];
@@ -1548,7 +1548,7 @@ __global__ void face_keys_kernel(const uint32_t* leaves, uint32_t n, const tv_te
         if (k[1] > k[2]) { uint32_t x = k[1]; k[1] = k[2]; k[2] = x; }
         if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
         const uint64_t o = 4ull * i + slot;
-        khi[o] = static_cast<uint64_t>(k[0]) << 32 | k[1];
+        khi[o] = static_cast<uint64_t>(k[0]) << vb | k[1];  // vertex ids < 2^vb: the sorts see 2 vb + vb bits
         klo[o] = k[2];
         rec[o] = static_cast<uint32_t>(o);
     }
@@ -1575,7 +1575,7 @@ __global__ void face_pair_kernel(const uint64_t* khi, const uint32_t* klo, const
 
 // face key of face record rec[p] (4 * leaf-list index + slot)
 __global__ void gather_face_hi_kernel(const uint32_t* rec, uint64_t n, const uint32_t* leaves, const tv_tet* tets,
-                                      uint64_t* khi, uint32_t* klo) {
+                                      uint64_t* khi, uint32_t* klo, int vb) {
     const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (p >= n) return;
     const uint32_t r = rec[p];
@@ -1588,7 +1588,7 @@ __global__ void gather_face_hi_kernel(const uint32_t* rec, uint64_t n, const uin
     if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
     if (k[1] > k[2]) { uint32_t x = k[1]; k[1] = k[2]; k[2] = x; }
     if (k[0] > k[1]) { uint32_t x = k[0]; k[0] = k[1]; k[1] = x; }
-    khi[p] = static_cast<uint64_t>(k[0]) << 32 | k[1];
+    khi[p] = static_cast<uint64_t>(k[0]) << vb | k[1];
     klo[p] = k[2];
 }
 
@@ -2326,29 +2326,31 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
         TRY(ensure(khi2, nf * 8));
         TRY(ensure(klo2, nf * 4));
         TRY(ensure(rec2, nf * 4));
+        int vb = 1;  // bits of a vertex id
+        while (vb < 32 && (1ull << vb) < n_v) ++vb;
         face_keys_kernel<<<nblk(n_leaves), 256>>>(leaves_b.as<uint32_t>(), n_leaves, tets_b.as<tv_tet>(),
-                                                  khi.as<uint64_t>(), klo.as<uint32_t>(), rec.as<uint32_t>());
+                                                  khi.as<uint64_t>(), klo.as<uint32_t>(), rec.as<uint32_t>(), vb);
         CK(cudaGetLastError(), "face keys");
         size_t tb1 = 0, tb2 = 0;
         CK(cub::DeviceRadixSort::SortPairs(nullptr, tb1, klo.as<uint32_t>(), klo2.as<uint32_t>(), rec.as<uint32_t>(),
-                                           rec2.as<uint32_t>(), static_cast<int>(nf)),
+                                           rec2.as<uint32_t>(), static_cast<int>(nf), 0, vb),
            "sort sizing");
         CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, khi.as<uint64_t>(), khi2.as<uint64_t>(), rec2.as<uint32_t>(),
-                                           rec.as<uint32_t>(), static_cast<int>(nf)),
+                                           rec.as<uint32_t>(), static_cast<int>(nf), 0, 2 * vb),
            "sort sizing");
         TRY(ensure(tmp_b, std::max(tb1, tb2)));
         // sort by v2, gather v0v1 in that order, then stable sort by v0v1
         CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb1, klo.as<uint32_t>(), klo2.as<uint32_t>(), rec.as<uint32_t>(),
-                                           rec2.as<uint32_t>(), static_cast<int>(nf)),
+                                           rec2.as<uint32_t>(), static_cast<int>(nf), 0, vb),
            "face sort lo");
         gather_face_hi_kernel<<<nblk(nf), 256>>>(rec2.as<uint32_t>(), nf, leaves_b.as<uint32_t>(), tets_b.as<tv_tet>(),
-                                                 khi.as<uint64_t>(), klo.as<uint32_t>());
+                                                 khi.as<uint64_t>(), klo.as<uint32_t>(), vb);
         CK(cudaGetLastError(), "face gather");
         CK(cub::DeviceRadixSort::SortPairs(tmp_b.p, tb2, khi.as<uint64_t>(), khi2.as<uint64_t>(), rec2.as<uint32_t>(),
-                                           rec.as<uint32_t>(), static_cast<int>(nf)),
+                                           rec.as<uint32_t>(), static_cast<int>(nf), 0, 2 * vb),
            "face sort hi");
         gather_face_hi_kernel<<<nblk(nf), 256>>>(rec.as<uint32_t>(), nf, leaves_b.as<uint32_t>(), tets_b.as<tv_tet>(),
-                                                 khi2.as<uint64_t>(), klo2.as<uint32_t>());
+                                                 khi2.as<uint64_t>(), klo2.as<uint32_t>(), vb);
         face_pair_kernel<<<nblk(nf), 256>>>(khi2.as<uint64_t>(), klo2.as<uint32_t>(), rec.as<uint32_t>(), nf,
                                             leaves_b.as<uint32_t>(), tets_b.as<tv_tet>(), d_err);
         CK(cudaGetLastError(), "face pair");
