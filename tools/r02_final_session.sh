@@ -1,10 +1,11 @@
 #!/bin/bash
 # Dev tool: the round-2 validation session (all GPU tests, smoke, bench, reference arm, profiles/ capture, C4 configs).
 cd $GRAFT_REPO_ROOT
-timeout 1800 python -m pytest -q -m gpu tests > gpurun_out/fin_tests.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/fin_smoke.log
-timeout 900 python bench.py > gpurun_out/fin_bench.log 2>&1
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/fin_ref.log 2>&1
+timeout 1800 python -m pytest -q -m gpu tests > gpurun_out/fin3_tests.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin3_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/fin3_smoke.log
+timeout 900 python bench.py > gpurun_out/fin3_bench.log 2>&1
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/fin3_ref.log 2>&1
 bash tools/profile_round.sh
-timeout 1500 python tools/configs_report.py c4 > gpurun_out/fin_c4.jsonl 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fin_c4_launches.csv python tools/build_repeat.py 1024 1.75 30 1 > gpurun_out/fin_c4_ncu.log 2>&1
+timeout 1500 python tools/configs_report.py c4 > gpurun_out/fin3_c4.jsonl 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/fin3_c4_launches.csv python tools/build_repeat.py 1024 1.75 30 1 > gpurun_out/fin3_c4_ncu.log 2>&1
+timeout 600 python tools/diag_ceiling.py gpurun_out/fin3_ceiling.json > gpurun_out/fin3_diag.log 2>&1
