@@ -117,6 +117,11 @@ def test_build_with_temperature_and_albedo(tv):
 def test_build_nonuniform_dims(tv):
     vol = np.ascontiguousarray(O.gen_volume("cloud", 48)[:, 5:37, 3:43])  # (48, 32, 40)
     check_same(tv, vol, O.build_cfg(0.3, 14, False, 1.0, 8.0))
+    # dims below and across the 8^3 brick size: only partial bricks on two axes
+    vol = np.ascontiguousarray(O.gen_volume("noise", 21)[:5, :7, :])  # (5, 7, 21)
+    check_same(tv, vol, O.build_cfg(0.1, 12, False, 1.0, 4.0))
+    vol = np.ascontiguousarray(O.gen_volume("blob", 40)[:, :, :33])  # (40, 40, 33)
+    check_same(tv, vol, O.build_cfg(0.2, 12, False, 1.0, 8.0))
 
 
 def test_build_config_errors(tv):
