@@ -144,11 +144,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
         : "memory");
 }
 
-template <bool TMA>
+template <int MODE>  // 0: load_leaf, 1: TMA bulk copies, 2: load_leaf_pair
 __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t* __restrict__ start,
                               const uint32_t* __restrict__ counts, const uint32_t* __restrict__ codes,
                               const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t regen_min,
                               uint32_t scatter_min, uint32_t* counter, uint32_t* sink) {
+    constexpr bool TMA = MODE == 1;
     extern __shared__ uint32_t pad[];  // the render's shared-memory footprint (L1 split, blocks per SM)
     __shared__ alignas(128) uint32_t rbuf[TMA ? 128 : 1][16];
     __shared__ alignas(8) unsigned long long mbar[TMA ? 128 : 1];
@@ -199,8 +200,8 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
                 k = 0;
                 n = counts[mine];
                 cw = codes + offs[mine];
-                idx = start[mine];
                 state = n ? STEP : IDLE;
+                if (n) idx = start[mine];  // (a path without steps may start at kNone)
             }
         }
         if (waiting && (static_cast<uint32_t>(__popc(waiting)) >= scatter_min || !stepping))
@@ -208,10 +209,20 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
         const unsigned run = __ballot_sync(kFull, state == STEP);
         if (!run) continue;
         for (;;) {
+            LeafRec rp;
+            if (MODE == 2) {
+                // a lane that is not stepping borrows its partner's index (no extra line)
+                const bool st = state == STEP;
+                const uint32_t pi = __shfl_xor_sync(kFull, idx, 1);
+                const bool pst = __shfl_xor_sync(kFull, st ? 1u : 0u, 1) != 0;
+                rp = load_leaf_pair(leaves, (!st && pst) ? pi : idx);
+            }
             if (state == STEP) {
                 if ((k & 7) == 0) word = cw[k >> 3];
                 LeafRec r;
-                if (TMA) {
+                if (MODE == 2) {
+                    r = rp;
+                } else if (TMA) {
                     const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
                     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&rbuf[threadIdx.x][0]));
                     bulk_load64(dst, leaves + idx, mb);
@@ -229,7 +240,10 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
                 const uint32_t code = (word >> (4 * (k & 7))) & 15u;
                 ++k;
                 // the next record's index comes out of this record (as in the render)
-                if (code < 4) idx = nbr_leaf(sel4(r.w[0], r.w[1], r.w[2], r.w[3], static_cast<int>(code)));
+                if (code < 4) {
+                    const uint32_t nx = nbr_leaf(sel4(r.w[0], r.w[1], r.w[2], r.w[3], static_cast<int>(code)));
+                    if (MODE != 2 || nx != kNoLeaf) idx = nx;  // (MODE 2: idle lanes keep a valid index)
+                }
                 if (k >= n) state = IDLE;
                 else if (code == 4) state = WAIT;  // collision: the scatter batch, then the same cell
             }
@@ -356,8 +370,9 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
     // what-if knobs (dev): shared-memory footprint per block and carveout of the first replay
     if (const char* v = std::getenv("TV_DIAG_SMEM")) trace_smem = static_cast<size_t>(std::atol(v));
     const bool tma = std::getenv("TV_DIAG_TMA") && std::atoi(std::getenv("TV_DIAG_TMA")) > 0;
-    const void* rk = tma ? reinterpret_cast<const void*>(replay_kernel<true>)
-                         : reinterpret_cast<const void*>(replay_kernel<false>);
+    const bool pair = std::getenv("TV_DIAG_PAIR") && std::atoi(std::getenv("TV_DIAG_PAIR")) > 0;
+    auto rkf = tma ? replay_kernel<1> : pair ? replay_kernel<2> : replay_kernel<0>;
+    const void* rk = reinterpret_cast<const void*>(rkf);
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trace_smem));
     const char* cv_env = std::getenv("TV_DIAG_CARVEOUT") ? std::getenv("TV_DIAG_CARVEOUT") : std::getenv("TV_CARVEOUT");
     cudaFuncSetAttribute(rk, cudaFuncAttributePreferredSharedMemoryCarveout, cv_env && *cv_env ? std::atoi(cv_env) : 72);
@@ -382,7 +397,7 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
         for (int r = 0; r < std::max(reps, 1); ++r) {
             CK(cudaMemset(ctr.p, 0, 256), "diag");
             cudaEventRecord(e0);
-            (tma ? replay_kernel<true> : replay_kernel<false>)<<<blocks, 128, smem>>>(g.leaves, static_cast<const uint32_t*>(cells.p),
+            rkf<<<blocks, 128, smem>>>(g.leaves, static_cast<const uint32_t*>(cells.p),
                                                  static_cast<const uint32_t*>(counts.p),
                                                  static_cast<const uint32_t*>(seq.p),
                                                  static_cast<const uint64_t*>(offs.p), B.n_paths, regen_min,
