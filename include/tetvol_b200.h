@@ -367,6 +367,31 @@ int tv_march_transmittance(const tv_grid* g, const tv_ray* rays, uint64_t n, dou
 /* sample_free_path (tracer.hpp:63) per ray with RngStream(seed, pixels[i], samples[i]). */
 int tv_sample_free_path(const tv_grid* g, const tv_ray* rays, uint64_t n, uint64_t seed, const uint64_t* pixels,
                         const uint64_t* samples, tv_free_path* out, uint64_t stats[2]);
+/* -- free-flight estimators over the per-tet majorant (optional modes) ------------
+ * The reference (and tv_render) uses regular tracking: one draw per flight and
+ * the exact optical depth of every crossed tet (path_integrator.hpp:49-61).
+ * Delta tracking samples tentative collisions at the per-tet majorant
+ * mu = majorant_scale * density (majorant_scale >= 1) and accepts each with
+ * probability density / mu; ratio tracking (transmittance only: the reference
+ * has no next-event estimation) weights the ray by 1 - density / mu per
+ * tentative collision. Both agree with regular tracking in distribution, not
+ * bit for bit (they draw the path's RngStream in their own order). */
+#define TV_TRACK_REGULAR 0
+#define TV_TRACK_DELTA 1
+#define TV_TRACK_RATIO 2
+/* render() with the given tracking (TV_TRACK_REGULAR: exactly tv_render;
+ * TV_TRACK_RATIO: TV_ERR_CONFIG). Same sample keys, camera jitter and
+ * ImageAccumulator outputs as tv_render. */
+int tv_render_tracking(const tv_grid* g, const tv_camera* camera, const tv_render_config* cfg, int32_t tracking,
+                       double majorant_scale, tv_framebuffer* out, tv_render_stats* stats);
+/* One transmittance estimate per ray over [t_min, t_max] with
+ * RngStream(seed, pixels[i], samples[i]): TV_TRACK_REGULAR gives exp(-tau)
+ * (march_transmittance, tracer.hpp:52; pixels / samples unused), DELTA 0 or 1,
+ * RATIO the ratio-tracking weight. stats: cells_visited, degenerate_paths. */
+int tv_transmittance_tracking(const tv_grid* g, const tv_ray* rays, uint64_t n, int32_t tracking,
+                              double majorant_scale, uint64_t seed, const uint64_t* pixels, const uint64_t* samples,
+                              double* trans_out, uint64_t stats[2]);
+
 /* points: 3*n doubles; out: reference TetIds (TV_NO_TET when outside). */
 int tv_locate_points(const tv_grid* g, const double* points, uint64_t n, uint32_t* out);
 

@@ -176,6 +176,10 @@ _sig("tv_locate_points", C.c_int, _P, _D, C.c_uint64, _U32)
 _sig("tv_march_transmittance", C.c_int, _P, _P, C.c_uint64, _D, _D, _U64)
 _sig("tv_trace_rays", C.c_int, _P, _P, C.c_uint64, C.POINTER(_RenderConfig), C.c_uint64, _U64, _U64, _D, _U64)
 _sig("tv_sample_free_path", C.c_int, _P, _P, C.c_uint64, C.c_uint64, _U64, _U64, _P, _U64)
+_sig("tv_render_tracking", C.c_int, _P, C.POINTER(_Camera), C.POINTER(_RenderConfig), C.c_int32, C.c_double,
+     C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
+_sig("tv_transmittance_tracking", C.c_int, _P, _P, C.c_uint64, C.c_int32, C.c_double, C.c_uint64, _U64, _U64, _D,
+     _U64)
 _sig("tv_render_regular", C.c_int, _F, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
      C.POINTER(_RenderConfig), C.c_int, C.POINTER(_Framebuffer), C.POINTER(_RenderStats))
 _sig("tv_render_regular_dev", C.c_int, _P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.POINTER(_Camera),
@@ -546,6 +550,41 @@ def march_transmittance(grid: TetGrid, rays: np.ndarray):
     _check(_lib.tv_march_transmittance(grid.handle, r.ctypes.data_as(_P), len(r), tau.ctypes.data_as(_D),
                                        tr.ctypes.data_as(_D), st.ctypes.data_as(_U64)))
     return tau, tr, int(st[0]), int(st[1])
+
+
+# free-flight estimators (include/tetvol_b200.h): regular tracking is the
+# reference's and tv_render's; delta / ratio tracking over the per-tet majorant
+# mu = majorant_scale * density are optional modes, equal in distribution
+TRACK_REGULAR, TRACK_DELTA, TRACK_RATIO = 0, 1, 2
+
+
+def render_tracking(grid: TetGrid, camera: PinholeCamera, cfg: RenderConfig, tracking: int = TRACK_DELTA,
+                    majorant_scale: float = 1.0) -> ImageAccumulator:
+    """render() with delta tracking over the per-tet majorant (TRACK_REGULAR is render())."""
+    w, h = int(camera.width), int(camera.height)
+    s = np.zeros(w * h * 3)
+    sq = np.zeros(w * h * 3)
+    cnt = np.zeros(w * h, np.uint32)
+    fb = _Framebuffer(s.ctypes.data_as(_D), sq.ctypes.data_as(_D), cnt.ctypes.data_as(_U32))
+    st = _RenderStats()
+    cam, rc = camera._c(), cfg._c()
+    _check(_lib.tv_render_tracking(grid.handle, C.byref(cam), C.byref(rc), int(tracking), float(majorant_scale),
+                                   C.byref(fb), C.byref(st)))
+    return ImageAccumulator(w, h, s, sq, cnt, st.cells_visited, st.paths_traced, st.degenerate_paths, st.seconds)
+
+
+def transmittance_tracking(grid: TetGrid, rays: np.ndarray, tracking: int, majorant_scale: float = 1.0,
+                           seed: int = 0, pixels=0, samples=0):
+    """One transmittance estimate per ray -> (estimates, cells_visited, degenerate_paths)."""
+    r = np.ascontiguousarray(rays, np.float64).reshape(-1, 8)
+    px = np.ascontiguousarray(np.broadcast_to(pixels, len(r)), np.uint64)
+    sm = np.ascontiguousarray(np.broadcast_to(samples, len(r)), np.uint64)
+    out = np.zeros(len(r))
+    st = np.zeros(2, np.uint64)
+    _check(_lib.tv_transmittance_tracking(grid.handle, r.ctypes.data_as(_P), len(r), int(tracking),
+                                          float(majorant_scale), int(seed), px.ctypes.data_as(_U64),
+                                          sm.ctypes.data_as(_U64), out.ctypes.data_as(_D), st.ctypes.data_as(_U64)))
+    return out, int(st[0]), int(st[1])
 
 
 def sample_free_path(grid: TetGrid, rays: np.ndarray, seed: int, pixels, samples):
