@@ -1416,10 +1416,26 @@ __global__ void bisect_kernel(const uint32_t* marked, uint32_t n, uint32_t n_t, 
 // made by the last bisect pass (ids >= first_new) and older leaves with at
 // least two vertices touched by that pass (a new midpoint lies on an edge of the
 // bisected tet, whose two endpoints were touched).
-__global__ void hanging_kernel(uint32_t n_t, uint32_t first_new, const uint4* __restrict__ tv4,
+// t0 > 0 (the probe path below): only the ids from t0 up, the new children.
+__device__ __forceinline__ bool has_hanging_edge(const uint4* __restrict__ verts, const HSlot* __restrict__ table,
+                                                 uint64_t mask, uint4 tv) {
+    const uint4 q[4] = {verts[tv.x], verts[tv.y], verts[tv.z], verts[tv.w]};
+    for (int e = 0; e < 6; ++e) {
+        const uint4 a = q[ep0(e)], b = q[ep1(e)];
+        const uint64_t sx = static_cast<uint64_t>(a.x) + b.x, sy = static_cast<uint64_t>(a.y) + b.y,
+                       sz = static_cast<uint64_t>(a.z) + b.z;
+        if ((sx | sy | sz) & 1u) continue;
+        if (hash_find(table, mask, verts, static_cast<uint32_t>(sx / 2), static_cast<uint32_t>(sy / 2),
+                      static_cast<uint32_t>(sz / 2)) != kNone)
+            return true;
+    }
+    return false;
+}
+
+__global__ void hanging_kernel(uint32_t t0, uint32_t n_t, uint32_t first_new, const uint4* __restrict__ tv4,
                                const uint4* __restrict__ verts, const HSlot* __restrict__ table, uint64_t mask,
                                const uint32_t* __restrict__ vtouch, uint8_t* flags) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t t = t0 + blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_t) return;
     const uint8_t f = flags[t];
     if (!(f & F_LEAF)) return;
@@ -1428,18 +1444,62 @@ __global__ void hanging_kernel(uint32_t n_t, uint32_t first_new, const uint4* __
         auto bit = [&](uint32_t v) { return (__ldg(vtouch + (v >> 5)) >> (v & 31)) & 1u; };
         if (bit(tv.x) + bit(tv.y) + bit(tv.z) + bit(tv.w) < 2) return;
     }
-    uint4 q[4] = {verts[tv.x], verts[tv.y], verts[tv.z], verts[tv.w]};
-    for (int e = 0; e < 6; ++e) {
-        const uint4 a = q[ep0(e)], b = q[ep1(e)];
-        const uint64_t sx = static_cast<uint64_t>(a.x) + b.x, sy = static_cast<uint64_t>(a.y) + b.y,
-                       sz = static_cast<uint64_t>(a.z) + b.z;
-        if ((sx | sy | sz) & 1u) continue;
-        if (hash_find(table, mask, verts, static_cast<uint32_t>(sx / 2), static_cast<uint32_t>(sy / 2),
-                      static_cast<uint32_t>(sz / 2)) != kNone) {
-            flags[t] = f | F_MARK;
-            return;
-        }
-    }
+    if (has_hanging_edge(verts, table, mask, tv)) flags[t] = f | F_MARK;
+}
+
+// The hanging test of the old leaves for a pass with few bisections, without
+// scanning every tet id. An old leaf (id < first_new) gets a hanging edge in
+// this pass only from a midpoint created by it (earlier midpoints already
+// marked every leaf around their edge, and those were bisected), and only if
+// it contains that midpoint's edge (a, b): it lies in the ring of leaves around
+// the edge. Every ring leaf holds a wedge around the edge with a dihedral angle
+// of at least 45 degrees (LEB tets of the 24 cube roots come in three
+// similarity classes), and, near the midpoint m, everything within a fraction
+// of its edge lengths (shape-regular). So 32 points m + eps (cos th u + sin th
+// v), th = (k + 1/2) 2 pi / 32, u, v perpendicular to b - a and eps = |b - a|
+// / 64, put at least three points strictly inside every ring leaf, and the
+// tree descent of the build (root_of + descend: the reference's locate_point,
+// tet_grid.cpp:428-472) finds it. One thread per (bisected tet with a new
+// midpoint, direction). The found old leaves get the same exact test as in
+// hanging_kernel; TV_HANG_CHECK=1 compares the marks with the full scan.
+__global__ void hanging_probe_kernel(const uint32_t* marked, uint32_t n, const uint32_t* mid_vid, uint32_t n_v_old,
+                                     uint32_t first_new, const tv_tet* tets, const uint4* __restrict__ tv4,
+                                     const uint4* __restrict__ verts, const HSlot* __restrict__ table,
+                                     uint64_t mask, RootScan R, const NodeRec* split, uint8_t* flags) {
+    const uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    const uint32_t i = static_cast<uint32_t>(g >> 5), k = static_cast<uint32_t>(g & 31);
+    if (i >= n) return;
+    const uint32_t vm = mid_vid[i];
+    if (vm == kNone || vm < n_v_old) return;  // not a midpoint created by this pass
+    const tv_tet& parent = tets[marked[i]];
+    int s0, s1;
+    refinement_slots(parent, verts, s0, s1);
+    const d3 a = vpos(verts[parent.verts[s0]]), b = vpos(verts[parent.verts[s1]]);
+    const d3 m = vpos(verts[vm]);
+    const d3 e = sub(b, a);
+    const double len = sqrt(dot(e, e));
+    const d3 eh = mk(e.x / len, e.y / len, e.z / len);
+    // u: eh x (the axis least aligned with eh), v = eh x u
+    const double ax = fabs(eh.x), ay = fabs(eh.y), az = fabs(eh.z);
+    const d3 axis = (ax <= ay && ax <= az) ? mk(1, 0, 0) : (ay <= az ? mk(0, 1, 0) : mk(0, 0, 1));
+    d3 u = cross(eh, axis);
+    const double ul = sqrt(dot(u, u));
+    u = mk(u.x / ul, u.y / ul, u.z / ul);
+    const d3 v = cross(eh, u);
+    const double th = (static_cast<double>(k) + 0.5) * (6.283185307179586 / 32.0);
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double eps = len * (1.0 / 64.0);
+    const d3 p = add(m, mk(eps * (cs * u.x + sn * v.x), eps * (cs * u.y + sn * v.y), eps * (cs * u.z + sn * v.z)));
+    if (!(p.x > 1e-9 && p.y > 1e-9 && p.z > 1e-9 && p.x < 1.0 - 1e-9 && p.y < 1.0 - 1e-9 && p.z < 1.0 - 1e-9))
+        return;  // outside the cube: no leaf there (the ring is cut by the boundary)
+    uint32_t o = root_of(R, verts, p);
+    if (o == kNone) return;
+    if (!(flags[o] & F_LEAF)) o = descend(split, flags, o, p);
+    if (o >= first_new) return;  // a new child: hanging_kernel tests every one
+    const uint8_t f = flags[o];
+    if (f & F_MARK) return;
+    if (has_hanging_edge(verts, table, mask, tv4[o])) flags[o] = f | F_MARK;  // racing writers store the same byte
 }
 
 // The ids whose flag has `bit` set, in ascending order: two passes over the
@@ -2158,6 +2218,15 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
     };
 
     uint64_t crit = 0, bisections = 0, passes = 0, replays = 0;
+    // hanging test by probes around the new midpoints when a pass bisects fewer
+    // than 1 / TV_HANG_PROBE_COST of the tets (TV_HANG_PROBE=0: always the full
+    // scan; TV_HANG_CHECK=1: run both and fail the build if they differ)
+    static const bool hang_probe = !std::getenv("TV_HANG_PROBE") || std::atoi(std::getenv("TV_HANG_PROBE"));
+    static const uint64_t hang_probe_cost =
+        std::getenv("TV_HANG_PROBE_COST") ? std::max(1, std::atoi(std::getenv("TV_HANG_PROBE_COST"))) : 64;
+    static const bool hang_check = std::getenv("TV_HANG_CHECK") && std::atoi(std::getenv("TV_HANG_CHECK"));
+    bool hang_mismatch = false;
+    uint64_t probe_passes = 0;
     bool pend_clean = false;  // the pending-midpoint table has been cleared in this build
     int rounds = 0;
     uint32_t n_fresh = 24, n_marked = 0, n_leaves = 24;
@@ -2314,10 +2383,38 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
             bisections += n_marked;
             ++passes;
             if (verbose) ph[1] += since(tp), tp = now();
-            // hanging test over every tet id, then the marked list (ascending ids)
-            hanging_kernel<<<nblk(n_t), 256>>>(n_t, first_new, tv4_b.as<uint4>(), verts_b.as<uint4>(),
-                                               table_b.as<HSlot>(), hmask, vtouch_b.as<uint32_t>(),
-                                               flags_b.as<uint8_t>());
+            // hanging test, then the marked list (ascending ids): over every tet
+            // id, or, for a pass with few bisections, over the new children plus
+            // the old leaves around the pass's new midpoints (hanging_probe_kernel)
+            const bool probe = hang_probe && static_cast<uint64_t>(n_pass) * hang_probe_cost < first_new;
+            if (probe) {
+                hanging_kernel<<<nblk(n_t - first_new), 256>>>(first_new, n_t, first_new, tv4_b.as<uint4>(),
+                                                               verts_b.as<uint4>(), table_b.as<HSlot>(), hmask,
+                                                               vtouch_b.as<uint32_t>(), flags_b.as<uint8_t>());
+                hanging_probe_kernel<<<nblk(32ull * n_pass), 256>>>(
+                    marked_b.as<uint32_t>(), n_pass, mid_b.as<uint32_t>(), n_v, first_new, tets_b.as<tv_tet>(),
+                    tv4_b.as<uint4>(), verts_b.as<uint4>(), table_b.as<HSlot>(), hmask, R, split_b.as<NodeRec>(),
+                    flags_b.as<uint8_t>());
+                ++probe_passes;
+            }
+            if (!probe || hang_check) {
+                uint32_t n_probe_marks = 0;
+                if (probe) {  // TV_HANG_CHECK: the full scan must add no mark the probes missed
+                    TRY(select_tets(F_MARK, marked_b, &n_probe_marks));
+                }
+                hanging_kernel<<<nblk(n_t), 256>>>(0, n_t, first_new, tv4_b.as<uint4>(), verts_b.as<uint4>(),
+                                                   table_b.as<HSlot>(), hmask, vtouch_b.as<uint32_t>(),
+                                                   flags_b.as<uint8_t>());
+                if (probe) {
+                    uint32_t n_scan_marks = 0;
+                    TRY(select_tets(F_MARK, marked_b, &n_scan_marks));
+                    if (n_scan_marks != n_probe_marks) {
+                        std::fprintf(stderr, "tetvol_b200: TV_HANG_CHECK: probes marked %u leaves, the scan %u\n",
+                                     n_probe_marks, n_scan_marks);
+                        hang_mismatch = true;
+                    }
+                }
+            }
             CK(cudaGetLastError(), "hanging");
             if (verbose) ph[2] += since(tp), tp = now();
             TRY(select_tets(F_MARK, marked_b, nullptr));
@@ -2342,6 +2439,9 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
                                   since(t_round));
         mark();
     }
+    if (verbose) std::fprintf(stderr, "tetvol_b200: build: %llu of %llu closure passes took the probe hanging test\n",
+                              static_cast<unsigned long long>(probe_passes), static_cast<unsigned long long>(passes));
+    if (hang_mismatch) return set_error(TV_ERR, "TV_HANG_CHECK: probe hanging test differs from the full scan");
     if (herr) {
         if (herr & E_LEVEL) return set_error(TV_ERR_GRID, "bisect: level cap reached");
         if (herr & E_MIDPOINT) return set_error(TV_ERR_GRID, "bisect: midpoint not representable");

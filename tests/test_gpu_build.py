@@ -185,7 +185,10 @@ def test_build_scratch_allocators_agree(tv, tmp_path):
     growth is a move); TV_BUILD_NO_VMM=1 (cudaMalloc + copy); TV_BUILD_CACHE=0
     (fresh scratch per build); TV_BUILD_POISON=1 (every byte a build has not
     written reads 0x5A); TV_VOX_BRICKS=0 (per-voxel ownership sweeps instead
-    of 8^3 bricks). All give the same grid, byte for byte."""
+    of 8^3 bricks); TV_HANG_PROBE=0 (every closure pass scans all tet ids for
+    hanging edges) and TV_HANG_PROBE_COST=1 with TV_HANG_CHECK=1 (nearly every
+    pass finds them by probes around the new midpoints, and the build fails if
+    a full scan marks anything more). All give the same grid, byte for byte."""
     import os
     import subprocess
     import sys
@@ -201,7 +204,8 @@ def test_build_scratch_allocators_agree(tv, tmp_path):
     for name, env in [("vmm", {}), ("tight", {"TV_BUILD_VMM_TIGHT": "1"}), ("malloc", {"TV_BUILD_NO_VMM": "1"}),
                       ("nocache", {"TV_BUILD_CACHE": "0"}), ("poison", {"TV_BUILD_POISON": "1"}),
                       ("poison_tight", {"TV_BUILD_POISON": "1", "TV_BUILD_VMM_TIGHT": "1"}),
-                      ("no_bricks", {"TV_VOX_BRICKS": "0"})]:
+                      ("no_bricks", {"TV_VOX_BRICKS": "0"}), ("scan_hanging", {"TV_HANG_PROBE": "0"}),
+                      ("probe_hanging", {"TV_HANG_PROBE_COST": "1", "TV_HANG_CHECK": "1"})]:
         f = str(tmp_path / f"{name}.npz")
         e = dict(os.environ, **env)
         subprocess.run([sys.executable, "-c", code, f], check=True, env=e, timeout=300)
@@ -247,9 +251,9 @@ def test_build_bricks_match_per_voxel_sweep_cloud256(tv):
             "v, t, r = g.download(); h = hashlib.sha256(v.tobytes() + t.tobytes() + r.tobytes()).hexdigest(); "
             "print(h, s.leaf_count, s.rounds, s.criterion_splits, s.propagation_splits)" % root)
     outs = []
-    for env in ({}, {"TV_VOX_BRICKS": "0"}):
+    for env in ({}, {"TV_VOX_BRICKS": "0"}, {"TV_HANG_PROBE": "0"}, {"TV_HANG_PROBE_COST": "2", "TV_HANG_CHECK": "1"}):
         p = subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, **env), timeout=300,
                            capture_output=True, text=True)
         outs.append(p.stdout.strip().splitlines()[-1])
-    assert outs[0] == outs[1]
+    assert outs[0] == outs[1] == outs[2] == outs[3]
     assert int(outs[0].split()[1]) == 3840746
