@@ -1460,17 +1460,21 @@ __global__ void hanging_kernel(uint32_t t0, uint32_t n_t, uint32_t first_new, co
 // / 64, put at least three points strictly inside every ring leaf, and the
 // tree descent of the build (root_of + descend: the reference's locate_point,
 // tet_grid.cpp:428-472) finds it. One thread per (bisected tet with a new
-// midpoint, direction). The found old leaves get the same exact test as in
+// midpoint, direction; `creator` = midpoint_win_kernel's winner flags). The
+// found old leaves get the same exact test as in
 // hanging_kernel; TV_HANG_CHECK=1 compares the marks with the full scan.
-__global__ void hanging_probe_kernel(const uint32_t* marked, uint32_t n, const uint32_t* mid_vid, uint32_t n_v_old,
-                                     uint32_t first_new, const tv_tet* tets, const uint4* __restrict__ tv4,
+__global__ void hanging_probe_kernel(const uint32_t* marked, uint32_t n, const uint32_t* mid_vid,
+                                     const uint32_t* creator, uint32_t first_new, const tv_tet* tets, const uint4* __restrict__ tv4,
                                      const uint4* __restrict__ verts, const HSlot* __restrict__ table,
                                      uint64_t mask, RootScan R, const NodeRec* split, uint8_t* flags) {
     const uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     const uint32_t i = static_cast<uint32_t>(g >> 5), k = static_cast<uint32_t>(g & 31);
     if (i >= n) return;
+    // only the bisection that created a new midpoint probes around it (the
+    // other ring members bisected in this pass share the edge)
+    if (!creator[i]) return;
     const uint32_t vm = mid_vid[i];
-    if (vm == kNone || vm < n_v_old) return;  // not a midpoint created by this pass
+    if (vm == kNone) return;
     const tv_tet& parent = tets[marked[i]];
     int s0, s1;
     refinement_slots(parent, verts, s0, s1);
@@ -2392,7 +2396,8 @@ int build_grid_impl(const float* dens, const float* temp, const float* alb, int 
                                                                verts_b.as<uint4>(), table_b.as<HSlot>(), hmask,
                                                                vtouch_b.as<uint32_t>(), flags_b.as<uint8_t>());
                 hanging_probe_kernel<<<nblk(32ull * n_pass), 256>>>(
-                    marked_b.as<uint32_t>(), n_pass, mid_b.as<uint32_t>(), n_v, first_new, tets_b.as<tv_tet>(),
+                    marked_b.as<uint32_t>(), n_pass, mid_b.as<uint32_t>(), head_b.as<uint32_t>(), first_new,
+                    tets_b.as<tv_tet>(),
                     tv4_b.as<uint4>(), verts_b.as<uint4>(), table_b.as<HSlot>(), hmask, R, split_b.as<NodeRec>(),
                     flags_b.as<uint8_t>());
                 ++probe_passes;
