@@ -144,7 +144,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
         : "memory");
 }
 
-template <int MODE>  // 0: load_leaf, 1: TMA bulk copies, 2: load_leaf_pair
+template <int MODE>  // 0: load_leaf, 1: TMA bulk copies, 2: load_leaf_pair, 3: 32-B half records
 __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t* __restrict__ start,
                               const uint32_t* __restrict__ counts, const uint32_t* __restrict__ codes,
                               const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t regen_min,
@@ -222,6 +222,12 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
                 LeafRec r;
                 if (MODE == 2) {
                     r = rp;
+                } else if (MODE == 3) {
+                    // what-if: a 32-B record (the first half only: the neighbour words)
+                    uint32_t h[8];
+                    ld256_na(leaves + idx, h);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) r.w[q] = h[q], r.w[8 + q] = h[q];
                 } else if (TMA) {
                     const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[threadIdx.x]));
                     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&rbuf[threadIdx.x][0]));
@@ -371,7 +377,8 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
     if (const char* v = std::getenv("TV_DIAG_SMEM")) trace_smem = static_cast<size_t>(std::atol(v));
     const bool tma = std::getenv("TV_DIAG_TMA") && std::atoi(std::getenv("TV_DIAG_TMA")) > 0;
     const bool pair = std::getenv("TV_DIAG_PAIR") && std::atoi(std::getenv("TV_DIAG_PAIR")) > 0;
-    auto rkf = tma ? replay_kernel<1> : pair ? replay_kernel<2> : replay_kernel<0>;
+    const bool half = std::getenv("TV_DIAG_HALF") && std::atoi(std::getenv("TV_DIAG_HALF")) > 0;
+    auto rkf = tma ? replay_kernel<1> : pair ? replay_kernel<2> : half ? replay_kernel<3> : replay_kernel<0>;
     const void* rk = reinterpret_cast<const void*>(rkf);
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trace_smem));
     const char* cv_env = std::getenv("TV_DIAG_CARVEOUT") ? std::getenv("TV_DIAG_CARVEOUT") : std::getenv("TV_CARVEOUT");
