@@ -257,3 +257,28 @@ def test_build_bricks_match_per_voxel_sweep_cloud256(tv):
         outs.append(p.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1] == outs[2] == outs[3]
     assert int(outs[0].split()[1]) == 3840746
+
+
+def test_build_probe_hanging_test_matches_scan_on_other_fields(tv):
+    """The probe hanging test (csrc/tv_build.cu, hanging_probe_kernel) forced on
+    every closure pass, with TV_HANG_CHECK=1 (the build fails if the full scan
+    marks anything more), on fields other than the cloud: value noise without a
+    camera and a step field; the grid equals the default build's byte for byte."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r); import oracle as O, paper_2506_11510_b200 as tv; "
+            "out = []\n"
+            "for kind, n, thr, ml in (('noise', 96, 0.05, 16), ('step', 64, 0.1, 14), ('ramp', 48, 0.02, 15)):\n"
+            "    g, s = tv.build_adaptive_grid(O.gen_volume(kind, n), tv.BuildConfig(thr, ml, False, 1.0, 4.0))\n"
+            "    v, t, r = g.download(); out.append(hashlib.sha256(v.tobytes() + t.tobytes()).hexdigest()[:16] + ':' + str(s.leaf_count))\n"
+            "print(' '.join(out))" % root)
+    outs = []
+    for env in ({"TV_HANG_PROBE": "0"}, {"TV_HANG_PROBE_COST": "1", "TV_HANG_CHECK": "1"}, {}):
+        p = subprocess.run([sys.executable, "-c", code], check=True, env=dict(os.environ, **env), timeout=300,
+                           capture_output=True, text=True)
+        outs.append(p.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1] == outs[2], outs

@@ -131,3 +131,33 @@ def test_tracking_errors(tv):
         tv.transmittance_tracking(vac, O.random_cube_rays(1, 1, 4), 7)
     with pytest.raises(tv.ConfigError):
         tv.render_tracking(vac, cam, tv.RenderConfig(spp=0), tv.TRACK_DELTA)
+
+
+def test_delta_render_emission_albedo_in_distribution(tv):
+    """Delta tracking with per-cell albedo and temperature emission (mask bits 2,
+    4) on a fuzzed grid, against the oracle's regular-tracking render."""
+    C = O.c_oracle()
+    g = O.fuzzed(C, 300, 0x77)
+    p = g.pools()
+    rng = np.random.default_rng(5)
+    leaf = p.leaf_mask
+    p.tets["density"][leaf] = rng.random(leaf.sum()).astype(np.float32) * 6
+    p.tets["temperature"][leaf] = rng.random(leaf.sum()).astype(np.float32) * 1.2
+    p.tets["albedo"][leaf] = rng.random(leaf.sum()).astype(np.float32)
+    p.tets["mask"][leaf] = 7
+    g2 = O.from_pools(C, p)
+    dg = tv.TetGrid.upload(p.vq, p.tets.view(tv.TET_DTYPE), p.roots, p.max_level)
+    w, h, spp = 48, 36, 128
+    kw = dict(spp=spp, max_bounces=16, seed=3, emission_scale=2.0, hg_g=-0.4)
+    cam = ((0.2, 0.7, -1.5), (0.1, -0.1, 1), (0, 1, 0), 50, w, h)
+    a = g2.render(O.camera(*cam), O.render_cfg(**kw), 0)
+    b = tv.render_tracking(dg, tv.PinholeCamera(*cam), tv.RenderConfig(**kw), tv.TRACK_DELTA, 2.0)
+    ma, mb = a["sum"] / spp, b.sum / spp
+    va = np.maximum(a["sum_sq"] / spp - ma * ma, 0) / spp
+    vb = np.maximum(b.sum_sq / spp - mb * mb, 0) / spp
+    se = np.sqrt(va + vb)
+    live = se > 0
+    assert np.array_equal(ma[~live], mb[~live])
+    z = (mb[live] - ma[live]) / se[live]
+    assert np.mean(np.abs(z) > 3.0) < 0.015, np.mean(np.abs(z) > 3.0)
+    assert abs(mb.mean() - ma.mean()) < 4 * np.sqrt((va + vb).sum()) / ma.size
