@@ -166,6 +166,8 @@ struct Workspace {
     int trace_blocks = 0, sms = 0;
     TraceFn trace = nullptr;
     int trace_threads = kTraceThreads;
+    TraceFn trace_hot = nullptr;  // the same kernel on the grid's 32-B hot records (DeviceGrid::hot)
+    int trace_blocks_hot = 0;
     uint32_t regen_min = 8, scatter_min = 8, order = 0;
     uint32_t tail_chunk = kChunk, tail_warps_x = 2;  // tail claims: size, and the zone in chunks per warp
     std::vector<cudaEvent_t> tev;  // per-batch kernel boundaries of the last frame (4 per batch)
@@ -297,6 +299,7 @@ int workspace(int device, Workspace*& out) {
         // tuning knobs (defaults are the measured best on B200)
         const int maxreg = env_int("TV_TRACE_MAXREG", 72);
         w.trace = trace_variant(maxreg, env_int("TV_TRACE_THREADS", 128), w.trace_threads);
+        w.trace_hot = trace_variant(maxreg, env_int("TV_TRACE_THREADS", 128), w.trace_threads, true);
         w.regen_min = static_cast<uint32_t>(env_int("TV_REGEN_MIN", 5));
         w.scatter_min = static_cast<uint32_t>(env_int("TV_SCATTER_MIN", 2));
         w.order = static_cast<uint32_t>(env_int("TV_ORDER", 1));
@@ -304,13 +307,18 @@ int workspace(int device, Workspace*& out) {
         w.tail_warps_x = static_cast<uint32_t>(std::max(env_int("TV_TAIL_ZONE", 2), 0));
         w.tile_mode = env_int("TV_TILE_ORDER", 1);
         w.tile_radius = env_int("TV_TILE_RADIUS_PCT", 80) / 100.0;
-        int per_sm = 1;
+        int per_sm = 1, per_sm_hot = 1;
         cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace), cudaFuncAttributePreferredSharedMemoryCarveout,
+                             env_int("TV_CARVEOUT", 72));
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(w.trace_hot), cudaFuncAttributePreferredSharedMemoryCarveout,
                              env_int("TV_CARVEOUT", 72));
         cudaDeviceGetAttribute(&w.sms, cudaDevAttrMultiProcessorCount, device);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(w.trace),
                                                       w.trace_threads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_hot, reinterpret_cast<const void*>(w.trace_hot),
+                                                      w.trace_threads, 0);
         w.trace_blocks = w.sms * (per_sm < 1 ? 1 : per_sm);
+        w.trace_blocks_hot = w.sms * (per_sm_hot < 1 ? 1 : per_sm_hot);
         if (TV_COLD_GLOBAL)
             TV_CK(cudaMalloc(&w.cold, static_cast<size_t>(w.trace_blocks) * w.trace_threads * kColdBytes),
                   "cold state alloc");
@@ -381,7 +389,8 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         B.cold = w.cold;
         {
             // the last tail_warps_x chunks per resident warp are claimed tail_chunk at a time
-            const uint64_t zone = static_cast<uint64_t>(w.trace_blocks) * (w.trace_threads / 32) * kChunk * w.tail_warps_x;
+            const uint64_t zone = static_cast<uint64_t>(g.view.hot ? w.trace_blocks_hot : w.trace_blocks) *
+                                  (w.trace_threads / 32) * kChunk * w.tail_warps_x;
             B.tail_chunk = w.tail_chunk;
             B.tail_from = B.n_paths > zone ? static_cast<uint32_t>(B.n_paths - zone) : 0u;
         }
@@ -391,8 +400,12 @@ int render_frame(const DeviceGrid& g, const CamView& cv, const RenderParams& rp,
         TV_CK(cudaGetLastError(), "start_kernel launch");
         TV_CK(cudaMemsetAsync(w.counter, 0, sizeof(uint32_t), st), "memset counter");
         TV_CK(cudaEventRecord(ev[1], st), "event");
-        w.trace<<<w.trace_blocks, w.trace_threads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
-                                                          w.counter);
+        if (g.view.hot)  // one 32-B load per step (HotRec); else the 64-B LeafRecs
+            w.trace_hot<<<w.trace_blocks_hot, w.trace_threads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad,
+                                                                      out.stats, w.counter);
+        else
+            w.trace<<<w.trace_blocks, w.trace_threads, 0, st>>>(g.view, cv, rp, B, st_rec, cells, rad, out.stats,
+                                                              w.counter);
         TV_CK(cudaGetLastError(), "trace_kernel launch");
         TV_CK(cudaEventRecord(ev[2], st), "event");
         const unsigned ab = static_cast<unsigned>(std::min<uint64_t>((units * 32 + 127) / 128, w.sms * 16ull));

@@ -104,6 +104,54 @@ __global__ void leaves_kernel(const tv_tet* __restrict__ tets, const uint32_t* _
     if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(act) - 1)) atomicMax(max_depth, lv);
 }
 
+// HotRec of every leaf from its LeafRec (tv_internal.cuh). The eight plane-test
+// coordinates q (integers, q / 2^24 = the f32 value) are split per axis into
+// base + offset * 2^tz; a leaf whose values do not fit (offset > 7, base >=
+// 2^18) sets *fail and the grid renders from the LeafRecs.
+__global__ void hot_kernel(const LeafRec* __restrict__ leaves, uint64_t n_leaves, HotRec* out, int* fail) {
+    const uint64_t L = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (L >= n_leaves) return;
+    const LeafRec r = leaves[L];
+    uint32_t q[8], ax[8];
+    uint32_t mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu};
+    for (int f = 0; f < 4; ++f) {
+        const uint32_t c = (r.w[12] >> (6 * f)) & 31u;
+        q[2 * f] = static_cast<uint32_t>(__uint_as_float(r.w[4 + 2 * f]) * 16777216.0f);
+        q[2 * f + 1] = static_cast<uint32_t>(__uint_as_float(r.w[5 + 2 * f] & 0x7fffffffu) * 16777216.0f);
+        ax[2 * f] = (c & 1u) ? 1u : 0u;
+        ax[2 * f + 1] = (c & 2u) ? 2u : 1u;
+    }
+    for (int k = 0; k < 8; ++k) mn[ax[k]] = min(mn[ax[k]], q[k]);
+    for (int a = 0; a < 3; ++a)
+        if (mn[a] == 0xffffffffu) mn[a] = 0;
+    uint32_t D = 0;
+    for (int k = 0; k < 8; ++k) D |= q[k] - mn[ax[k]];
+    int tz = D ? __ffs(D) - 1 : 24;
+    for (int a = 0; a < 3; ++a)
+        if (mn[a]) tz = min(tz, __ffs(mn[a]) - 1);
+    bool ok = true;
+    uint32_t G = 0;
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t o = (q[k] - mn[ax[k]]) >> tz;
+        ok &= o <= 7u;
+        G |= (o & 7u) << (3 * k);
+    }
+    for (int a = 0; a < 3; ++a) ok &= (mn[a] >> tz) < (1u << 18);
+    HotRec h;
+    h.w[0] = r.w[0], h.w[1] = r.w[1], h.w[2] = r.w[2], h.w[3] = r.w[3];
+    h.w[4] = r.w[13];
+    h.w[5] = (mn[0] >> tz) | ((G & 0xfffu) << 18);
+    h.w[6] = (mn[1] >> tz) | ((G >> 12) << 18);
+    h.w[7] = (mn[2] >> tz) | (static_cast<uint32_t>(tz) << 18);
+    if (!ok) {
+        atomicOr(fail, 1);
+        for (int k = 0; k < 8; ++k) h.w[k] = 0;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + L);
+    dst[0] = make_uint4(h.w[0], h.w[1], h.w[2], h.w[3]);
+    dst[1] = make_uint4(h.w[4], h.w[5], h.w[6], h.w[7]);
+}
+
 // tet_grid.cpp:288-330 (exact integer longest edge; ties towards smaller ids)
 __device__ void refinement_slots(const tv_tet& tt, const uint4* verts, int& s0, int& s1) {
     int best = 0;
@@ -346,6 +394,30 @@ int finalize_grid(DeviceGrid& g, cudaStream_t st) {
     v.n_nodes = static_cast<uint32_t>(g.n_internal);
     v.jump = nullptr;
     v.jump_res = 0;
+    v.hot = nullptr;
+    v.code_lut = 0;
+    for (uint32_t k = 0; k < 9; ++k) v.code_lut |= static_cast<uint64_t>(pos2_code(2 * k)) << (5 * k);
+    {
+        // TV_HOT=1: 32-B hot records, one load per trace step. Measured slower
+        // on B200 (C2 frame 61.3 -> 70.4 ms): decoding the coordinates costs
+        // more issue slots than the halved L1 wavefronts save; off by default
+        const char* e = std::getenv("TV_HOT");
+        if (e && std::atoi(e) && g.n_leaves) {
+            TRY(dalloc(&g.hot, g.n_leaves, g.bytes));
+            CK(cudaMemsetAsync(d_depth, 0, sizeof(int), st), "hot flag");
+            hot_kernel<<<blocks(g.n_leaves, 256), 256, 0, st>>>(g.leaves, g.n_leaves, g.hot, d_depth);
+            CK(cudaGetLastError(), "hot_kernel");
+            int fail = 0;
+            CK(cudaMemcpyAsync(&fail, d_depth, sizeof(int), cudaMemcpyDeviceToHost, st), "hot flag D2H");
+            CK(cudaStreamSynchronize(st), "hot records");
+            if (fail) {
+                cudaFree(g.hot);
+                g.hot = nullptr;
+                g.bytes -= g.n_leaves * sizeof(HotRec);
+            }
+            v.hot = g.hot;
+        }
+    }
     {
         // TV_JUMP_RES: cubes per axis of the locate jump table (0 = none);
         // 128^3 entries = 8 MB
@@ -375,6 +447,8 @@ void free_grid(DeviceGrid& g) {
     cudaFree(g.leaf2tet);
     cudaFree(g.mask);
     cudaFree(g.jump);
+    cudaFree(g.hot);
+    g.hot = nullptr;
     g.jump = nullptr;
     g.mask = nullptr;
     g.tets = nullptr;

@@ -21,6 +21,8 @@
 //                 exactly the reference accumulation order
 //                 (path_integrator.hpp:109-114, image.hpp:36-45), so the
 //                 framebuffer is bit-comparable with the CPU reference.
+#include <type_traits>
+
 #include "tv_trace.cuh"
 
 namespace tvb {

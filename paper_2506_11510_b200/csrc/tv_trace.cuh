@@ -58,7 +58,7 @@ using TraceFn = void (*)(GridView, CamView, RenderParams, Batch, const StartRec*
                          uint64_t*, uint32_t*);
 // trace kernel instantiated for 4, 5, 6 or 8 resident blocks per SM
 // the trace kernel for a register cap and a number of path slots per lane
-TraceFn trace_variant(int maxreg, int block_threads, int& threads);
+TraceFn trace_variant(int maxreg, int block_threads, int& threads, bool hot = false);
 __global__ void accum_kernel(Batch B, CamView C, const uint32_t* cells, const double* rad, RenderOut O);
 __global__ void march_kernel(GridView G, const tv_ray* rays, uint64_t n, int pass, uint64_t* counts,
                              const uint64_t* offsets, tv_segment* out, uint64_t cap, unsigned long long* deg);
@@ -85,6 +85,7 @@ struct DeviceGrid {
     uint32_t* leaf2tet = nullptr;
     uint8_t* mask = nullptr;
     uint32_t* jump = nullptr;  // locate jump table (view.jump)
+    HotRec* hot = nullptr;     // 32-B hot records (view.hot; null when the geometry does not fit them)
     GridView view{};
     uint64_t bytes = 0;
 };

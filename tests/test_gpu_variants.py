@@ -1,6 +1,6 @@
 """Every selectable trace-kernel configuration (register cap, block size,
-warp-batching thresholds, path order, locate jump-table resolution; DESIGN.md
-§4 tuning knobs) renders the
+warp-batching thresholds, path order, locate jump-table resolution, 32-B hot
+records; DESIGN.md §4 tuning knobs) renders the
 same framebuffer bits: the knobs change scheduling, never results. Each
 configuration runs in a subprocess because the library reads the knobs once
 per process."""
@@ -30,6 +30,8 @@ CONFIGS = [
     {"TV_JUMP_RES": "0"},
     {"TV_JUMP_RES": "32"},
     {"TV_JUMP_RES": "256"},
+    {"TV_HOT": "1"},  # 32-B hot records (csrc/tv_grid.cu hot_kernel, exit_face_hot3)
+    {"TV_HOT": "1", "TV_TRACE_MAXREG": "96"},
 ]
 
 
