@@ -18,6 +18,7 @@
 //    Its steps/s is the rate of a trace kernel whose exit-face computation
 //    were free.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
 #include <vector>
@@ -144,7 +145,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
         : "memory");
 }
 
-template <int MODE>  // 0: load_leaf, 1: TMA bulk copies, 2: load_leaf_pair, 3: 32-B half records
+template <int MODE>  // 0: load_leaf, 1: TMA bulk copies, 2: load_leaf_pair, 3: 32-B half records, 4: count lines
 __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t* __restrict__ start,
                               const uint32_t* __restrict__ counts, const uint32_t* __restrict__ codes,
                               const uint64_t* __restrict__ offs, uint32_t n_paths, uint32_t regen_min,
@@ -168,6 +169,7 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
     uint32_t k = 0, n = 0;          // this lane's path: step k of n
     const uint32_t* cw = nullptr;   // its code words
     uint32_t idx = 0, word = 0, acc = 0;
+    unsigned long long n_lanes = 0, n_lines = 0;  // MODE 4
     for (;;) {
         const unsigned idle = __ballot_sync(kFull, state == IDLE);
         const unsigned stepping = __ballot_sync(kFull, state == STEP);
@@ -242,6 +244,12 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
                 } else {
                     r = load_leaf(leaves, idx);
                 }
+                if (MODE == 4) {  // what-if count: distinct 128-B record lines per warp load vs stepping lanes
+                    const unsigned act = __activemask();
+                    const unsigned peers = __match_any_sync(act, idx >> 1);
+                    n_lanes += 1;
+                    n_lines += (__ffs(peers) - 1) == lane ? 1u : 0u;
+                }
                 acc ^= r.w[5] ^ r.w[10] ^ r.w[15];
                 const uint32_t code = (word >> (4 * (k & 7))) & 15u;
                 ++k;
@@ -257,6 +265,10 @@ __global__ void replay_kernel(const LeafRec* __restrict__ leaves, const uint32_t
         }
     }
     if (acc == 0x9e3779b9u) sink[0] = acc + pad[0];  // keeps the loads alive
+    if (MODE == 4) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(sink) + 2, n_lanes);
+        atomicAdd(reinterpret_cast<unsigned long long*>(sink) + 3, n_lines);
+    }
 }
 
 // words of 4-bit codes per path
@@ -378,7 +390,9 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
     const bool tma = std::getenv("TV_DIAG_TMA") && std::atoi(std::getenv("TV_DIAG_TMA")) > 0;
     const bool pair = std::getenv("TV_DIAG_PAIR") && std::atoi(std::getenv("TV_DIAG_PAIR")) > 0;
     const bool half = std::getenv("TV_DIAG_HALF") && std::atoi(std::getenv("TV_DIAG_HALF")) > 0;
-    auto rkf = tma ? replay_kernel<1> : pair ? replay_kernel<2> : half ? replay_kernel<3> : replay_kernel<0>;
+    const bool count = std::getenv("TV_DIAG_COUNT") && std::atoi(std::getenv("TV_DIAG_COUNT")) > 0;
+    auto rkf = tma ? replay_kernel<1>
+                   : pair ? replay_kernel<2> : half ? replay_kernel<3> : count ? replay_kernel<4> : replay_kernel<0>;
     const void* rk = reinterpret_cast<const void*>(rkf);
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(trace_smem));
     const char* cv_env = std::getenv("TV_DIAG_CARVEOUT") ? std::getenv("TV_DIAG_CARVEOUT") : std::getenv("TV_CARVEOUT");
@@ -416,6 +430,13 @@ extern "C" int tv_diag_gather_ceiling(const tv_grid* h, const tv_camera* camera,
             float ms = 0.f;
             cudaEventElapsedTime(&ms, e0, e1);
             best[mode] = std::min(best[mode], static_cast<double>(ms));
+            if (count && r == 0) {
+                unsigned long long c[2];
+                cudaMemcpy(c, static_cast<char*>(ctr.p) + 144, sizeof(c), cudaMemcpyDeviceToHost);
+                std::fprintf(stderr, "tetvol_b200: diag replay (%s): %llu lane loads, %llu distinct record lines (%.3f)\n",
+                             mode == 0 ? "trace shape" : "full occupancy", c[0], c[1],
+                             c[0] ? static_cast<double>(c[1]) / c[0] : 0.0);
+            }
         }
     }
     cudaEventDestroy(e0);
